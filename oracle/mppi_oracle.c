@@ -1,0 +1,395 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of one MPPI iteration with a Gate-SDF cost
+ * (arxiv 2603.07199), written step by step in the paper's order. Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it. It shares no code, header, table
+ * or constant generator with the CUDA path under paper_2603_07199_b200/.
+ *
+ * Precision: every floating-point step is fp64, except the bf16 quantisation contract of BASELINE
+ * configs[1..4] ("bf16, fp32 accumulate"; SURVEY.md §8c reading R15), which is emulated exactly:
+ * hidden/output weights rounded once to bf16 (RNE), hidden activations rounded to bf16 after the
+ * activation. Those rounding decisions are taken on the fp32 value of the activation (the kernel's
+ * precision, as the task's rule for float-decides-integer asks).
+ *
+ * Citations (PAPER.md line, section/equation):
+ *   sampling      U^m = U* + dU^m, dU ~ N(0, Sigma)                PAPER.md:139 (§IV-A)
+ *   update        U* = sum w_m U^m, w = softmax(-J/lambda)         PAPER.md:140-144 (Eq. 5)
+ *   dynamics      xdot = f(x,u)                                    PAPER.md:146 (§IV-A), CTBR form of
+ *                 BASELINE configs[0] (state p,v,q; input thrust + body rates; RK4)
+ *   SDF query     s_k = g_phi(z, p_k), latent once per frame      PAPER.md:168 (§IV-B3)
+ *   cached frame  world -> cached camera transform                 PAPER.md:181 (§IV-B3)
+ *   total cost    J = sum of weighted stage costs                  PAPER.md:185 (Eq. 10), with the
+ *                 BASELINE configs[0..1] terms (||p-g_c||^2, 50 exp(-s/0.1), 0.01||u||^2, -0.5 grad s.v)
+ *   analytic SDF  s_guide = c + |x| tan(a) - max(|y|,|z|)          PAPER.md:64-72 (Eqs. 1-2)
+ *   noise RNG     Philox4x32-10 + Box-Muller (reading R24)        — parity unpinned against the paper
+ *                 (the paper draws N(0,Sigma) without naming a generator); pinned to the Random123 KAT.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ACT_SOFTPLUS 0
+#define ACT_RELU 1
+#define ACT_SILU 2
+
+typedef struct {
+    int32_t n_ctrl, K, T;
+    double dt, lambda, mass, gravity;
+    double u_lo[4], u_hi[4], sigma[4];
+    double w_goal, w_sdf, sdf_scale, sdf_exp_max, w_u, w_guide, fd_h;
+    int32_t latent_dim, hidden, n_hidden, activation, mlp_bf16;
+    int32_t sdf_mode;            /* 0: MLP g_phi; 1: analytic Gate-SDF (Eq. 2) in the query frame */
+    double gate_c, gate_tana;    /* analytic-SDF parameters (sdf_mode 1) */
+} oracle_cfg;
+
+/* ------------------------------------------------------------------ Philox4x32-10 (Salmon et al.) */
+static void philox_round(uint32_t c[4], const uint32_t k[2]) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0];
+    uint32_t n2 = hi0 ^ c[3] ^ k[1];
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    uint32_t k[2] = {key[0], key[1]};
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+        philox_round(c, k);
+    }
+    memcpy(out, c, sizeof(c));
+}
+
+/* Standard normals for global samples g0..g0+nK-1 (R24): key = seed, counter = (g, t, step_lo, step_hi);
+ * u_i = ((x_i >> 8) + 0.5) * 2^-24; Box-Muller on (u0,u1) -> n0,n1 and (u2,u3) -> n2,n3.
+ * out: [T][nK][4]. */
+void oracle_noise(uint64_t seed, uint64_t step, int64_t g0, int32_t nK, int32_t T, double* out) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int t = 0; t < T; ++t)
+        for (int i = 0; i < nK; ++i) {
+            uint64_t g = (uint64_t)(g0 + i);
+            uint32_t ctr[4] = {(uint32_t)g, (uint32_t)t, (uint32_t)step, (uint32_t)(step >> 32)};
+            uint32_t x[4];
+            oracle_philox4x32_10(ctr, key, x);
+            double u[4];
+            for (int j = 0; j < 4; ++j) u[j] = ((double)(x[j] >> 8) + 0.5) * (1.0 / 16777216.0);
+            double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
+            double* o = out + ((size_t)t * nK + i) * 4;
+            o[0] = r0 * cos(two_pi * u[1]);
+            o[1] = r0 * sin(two_pi * u[1]);
+            o[2] = r1 * cos(two_pi * u[3]);
+            o[3] = r1 * sin(two_pi * u[3]);
+        }
+}
+
+/* ------------------------------------------------------------------ bf16 round-to-nearest-even */
+static double bf16_round(double v) {
+    float f = (float)v;                       /* decision taken on the fp32 value (kernel precision) */
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u) {   /* inf / nan pass through (nan quieted) */
+        if (u & 0x007FFFFFu) u |= 0x00400000u;
+        u &= 0xFFFF0000u;
+    } else {
+        u += 0x7FFFu + ((u >> 16) & 1u);
+        u &= 0xFFFF0000u;
+    }
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+double oracle_bf16_round(double v) { return bf16_round(v); }
+
+/* ------------------------------------------------------------------ dynamics (CTBR, R1-R4) */
+/* x = [p(3), v(3), q(w,x,y,z)]; u = [c (N), wx, wy, wz (rad/s, body frame)].
+ * pdot = v; vdot = (c/m) b3(q) - g e_z with b3(q) = R(q) e_z; qdot = 1/2 q (x) (0, w). */
+static void dyn_f(const double* x, const double* u, double m, double g, double* xd) {
+    const double qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+    const double c = u[0], wx = u[1], wy = u[2], wz = u[3];
+    xd[0] = x[3]; xd[1] = x[4]; xd[2] = x[5];
+    const double b3x = 2.0 * (qx * qz + qw * qy);
+    const double b3y = 2.0 * (qy * qz - qw * qx);
+    const double b3z = 1.0 - 2.0 * (qx * qx + qy * qy);
+    xd[3] = c / m * b3x;
+    xd[4] = c / m * b3y;
+    xd[5] = c / m * b3z - g;
+    /* Hamilton product q (x) (0, w) */
+    xd[6] = 0.5 * (-qx * wx - qy * wy - qz * wz);
+    xd[7] = 0.5 * (qw * wx + qy * wz - qz * wy);
+    xd[8] = 0.5 * (qw * wy + qz * wx - qx * wz);
+    xd[9] = 0.5 * (qw * wz + qx * wy - qy * wx);
+}
+
+/* Classic RK4 with the input held over the step; q renormalised after the full step only (R4). */
+void oracle_rk4_step(const double* x, const double* u, double dt, double m, double g, double* out) {
+    double k1[10], k2[10], k3[10], k4[10], xt[10];
+    dyn_f(x, u, m, g, k1);
+    for (int i = 0; i < 10; ++i) xt[i] = x[i] + 0.5 * dt * k1[i];
+    dyn_f(xt, u, m, g, k2);
+    for (int i = 0; i < 10; ++i) xt[i] = x[i] + 0.5 * dt * k2[i];
+    dyn_f(xt, u, m, g, k3);
+    for (int i = 0; i < 10; ++i) xt[i] = x[i] + dt * k3[i];
+    dyn_f(xt, u, m, g, k4);
+    for (int i = 0; i < 10; ++i) out[i] = x[i] + dt / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    double qn = sqrt(out[6] * out[6] + out[7] * out[7] + out[8] * out[8] + out[9] * out[9]);
+    for (int i = 6; i < 10; ++i) out[i] /= qn;
+}
+
+/* ------------------------------------------------------------------ SDF providers */
+static double act_fn(int a, double v) {
+    switch (a) {
+        case ACT_SOFTPLUS: return (v > 0.0 ? v : 0.0) + log1p(exp(-fabs(v)));
+        case ACT_RELU: return v > 0.0 ? v : 0.0;
+        default: return v / (1.0 + exp(-v));   /* SiLU */
+    }
+}
+
+/* s = g_phi(z, p): layer 1 on [p | z] (full 3+L dot, fp64, NOT folded); hidden layers; linear output.
+ * W: all layers concatenated, each [out][in] row-major (nn.Linear); b likewise. */
+double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p) {
+    const int L = cfg->latent_dim, H = cfg->hidden;
+    double* a = (double*)malloc(sizeof(double) * (size_t)H);
+    double* an = (double*)malloc(sizeof(double) * (size_t)H);
+    const float* Wl = W;
+    const float* bl = b;
+    const int in1 = 3 + L;
+    for (int i = 0; i < H; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < 3; ++j) acc += (double)Wl[(size_t)i * in1 + j] * p[j];
+        for (int j = 0; j < L; ++j) acc += (double)Wl[(size_t)i * in1 + 3 + j] * (double)z[j];
+        acc += (double)bl[i];
+        double v = act_fn(cfg->activation, acc);
+        a[i] = cfg->mlp_bf16 ? bf16_round(v) : v;
+    }
+    Wl += (size_t)H * in1;
+    bl += H;
+    for (int l = 1; l < cfg->n_hidden; ++l) {
+        for (int i = 0; i < H; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < H; ++j) {
+                double w = (double)Wl[(size_t)i * H + j];
+                if (cfg->mlp_bf16) w = bf16_round(w);
+                acc += w * a[j];
+            }
+            acc += (double)bl[i];
+            double v = act_fn(cfg->activation, acc);
+            an[i] = cfg->mlp_bf16 ? bf16_round(v) : v;
+        }
+        memcpy(a, an, sizeof(double) * (size_t)H);
+        Wl += (size_t)H * H;
+        bl += H;
+    }
+    double s = 0.0;
+    for (int j = 0; j < H; ++j) {
+        double w = (double)Wl[j];
+        if (cfg->mlp_bf16) w = bf16_round(w);
+        s += w * a[j];
+    }
+    s += (double)bl[0];
+    free(a);
+    free(an);
+    return s;
+}
+
+/* Eq. 1-2: r(p) = max(|y|,|z|); s_guide = c + |x| tan(alpha) - r(p). */
+double oracle_sdf_analytic(double c, double tana, const double* p) {
+    double r = fabs(p[1]) > fabs(p[2]) ? fabs(p[1]) : fabs(p[2]);
+    return c + fabs(p[0]) * tana - r;
+}
+
+static double sdf_eval(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p) {
+    if (cfg->sdf_mode == 1) return oracle_sdf_analytic(cfg->gate_c, cfg->gate_tana, p);
+    return oracle_mlp(cfg, W, b, z, p);
+}
+
+/* MLP on externally given query-frame rows [n][4] (x,y,z,_) -> s[n] (test support). */
+void oracle_sdf_rows(const oracle_cfg* cfg, const float* W, const float* b, const float* z,
+                     const float* rows, int64_t n, double* out) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) {
+        double p[3] = {rows[i * 4 + 0], rows[i * 4 + 1], rows[i * 4 + 2]};
+        out[i] = sdf_eval(cfg, W, b, z, p);
+    }
+}
+
+/* ------------------------------------------------------------------ rollout + cost of one sample */
+static double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* One sample: u_t = clamp(U*_t + sigma * n_t) (clamp per R5); x_{t+1} = RK4(x_t, u_t);
+ * query at x_{t+1} (R7) in the cached frame p_c = R p + t; SDF s = g_phi(z, p_c)
+ * (PAPER.md:168); guidance by directional forward difference along d = R v / |v| (R12);
+ * stage cost c_t = w_goal |p - g_c|^2 + w_sdf exp(min(-s/scale, emax)) + w_u |u|^2
+ *                 - w_guide |v| (s(p_c + h d) - s(p_c)) / h       (Eq. 10 structure; BASELINE terms);
+ * J = sum_t c_t, non-finite -> +inf.
+ * noise: [T] x 4 with element stride `nstride` between time steps. Outputs may be NULL:
+ * states [T+1][10], queries [T][8] (p_c, |v|, p_c + h d, 0), sdf [T][2], stage [T]. */
+double oracle_rollout(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const float* Tq,
+                      const float* x0, const float* goal, const float* U, const double* noise, int64_t nstride,
+                      double* states, double* queries, double* sdf, double* stage) {
+    const int T = cfg->T;
+    double x[10], xn[10], u[4];
+    for (int i = 0; i < 10; ++i) x[i] = x0[i];
+    if (states) memcpy(states, x, sizeof(x));
+    double J = 0.0;
+    const int guide = cfg->w_guide != 0.0;
+    for (int t = 0; t < T; ++t) {
+        const double* n = noise + (size_t)t * nstride;
+        for (int c = 0; c < 4; ++c) u[c] = clampd((double)U[t * 4 + c] + cfg->sigma[c] * n[c], cfg->u_lo[c], cfg->u_hi[c]);
+        oracle_rk4_step(x, u, cfg->dt, cfg->mass, cfg->gravity, xn);
+        memcpy(x, xn, sizeof(x));
+        if (states) memcpy(states + (size_t)(t + 1) * 10, x, sizeof(x));
+        const double* p = x;
+        const double* v = x + 3;
+        double pc[3], dv[3], pc2[3];
+        for (int r = 0; r < 3; ++r) {
+            pc[r] = (double)Tq[r * 3 + 0] * p[0] + (double)Tq[r * 3 + 1] * p[1] + (double)Tq[r * 3 + 2] * p[2] + (double)Tq[9 + r];
+            dv[r] = (double)Tq[r * 3 + 0] * v[0] + (double)Tq[r * 3 + 1] * v[1] + (double)Tq[r * 3 + 2] * v[2];
+        }
+        const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        for (int r = 0; r < 3; ++r) pc2[r] = pc[r] + cfg->fd_h * (nv >= 1e-6 ? dv[r] / nv : 0.0);
+        const double s0 = sdf_eval(cfg, W, b, z, pc);
+        const double s1 = guide ? sdf_eval(cfg, W, b, z, pc2) : s0;
+        double dg = 0.0;
+        for (int r = 0; r < 3; ++r) dg += (p[r] - (double)goal[r]) * (p[r] - (double)goal[r]);
+        double un = u[0] * u[0] + u[1] * u[1] + u[2] * u[2] + u[3] * u[3];
+        double ex = -s0 / cfg->sdf_scale;
+        if (ex > cfg->sdf_exp_max) ex = cfg->sdf_exp_max;
+        double ct = cfg->w_goal * dg + cfg->w_sdf * exp(ex) + cfg->w_u * un;
+        if (guide) ct -= cfg->w_guide * nv * (s1 - s0) / cfg->fd_h;
+        if (queries) {
+            double* q = queries + (size_t)t * 8;
+            q[0] = pc[0]; q[1] = pc[1]; q[2] = pc[2]; q[3] = nv;
+            q[4] = pc2[0]; q[5] = pc2[1]; q[6] = pc2[2]; q[7] = 0.0;
+        }
+        if (sdf) { sdf[t * 2] = s0; sdf[t * 2 + 1] = s1; }
+        if (stage) stage[t] = ct;
+        J += ct;
+    }
+    if (!isfinite(J)) J = INFINITY;
+    return J;
+}
+
+/* ------------------------------------------------------------------ softmin update (Eq. 5) */
+/* For one controller: J[K]; U[T][4]; noise with element stride nstride between t and 4 between k.
+ * Jmin = min J; w_k = exp(-(J_k - Jmin)/lambda); S = sum w; V_t = sum_k w_k (u_{k,t} - U_t);
+ * U_new = U + V/S. All J infinite -> U_new = U, flag 1 (SPEC.md:341 reading). */
+int oracle_softmin(const oracle_cfg* cfg, int32_t K, const double* J, const float* U, const double* noise,
+                   int64_t nstride, double* Jmin_o, double* S_o, double* V, double* U_new, double* ess_o) {
+    const int T = cfg->T;
+    double Jmin = INFINITY;
+    for (int k = 0; k < K; ++k) if (J[k] < Jmin) Jmin = J[k];
+    for (int i = 0; i < T * 4; ++i) V[i] = 0.0;
+    if (!(Jmin < INFINITY)) {
+        for (int i = 0; i < T * 4; ++i) U_new[i] = U[i];
+        if (Jmin_o) *Jmin_o = INFINITY;
+        if (S_o) *S_o = 0.0;
+        if (ess_o) *ess_o = 0.0;
+        return 1;
+    }
+    double S = 0.0, S2 = 0.0;
+    for (int k = 0; k < K; ++k) {
+        double w = (J[k] < INFINITY) ? exp(-(J[k] - Jmin) / cfg->lambda) : 0.0;
+        S += w;
+        S2 += w * w;
+        if (w == 0.0) continue;
+        for (int t = 0; t < T; ++t)
+            for (int c = 0; c < 4; ++c) {
+                double uk = clampd((double)U[t * 4 + c] + cfg->sigma[c] * noise[(size_t)t * nstride + (size_t)k * 4 + c],
+                                   cfg->u_lo[c], cfg->u_hi[c]);
+                V[t * 4 + c] += w * (uk - (double)U[t * 4 + c]);
+            }
+    }
+    for (int i = 0; i < T * 4; ++i) U_new[i] = (double)U[i] + V[i] / S;
+    if (Jmin_o) *Jmin_o = Jmin;
+    if (S_o) *S_o = S;
+    if (ess_o) *ess_o = S * S / S2;
+    return 0;
+}
+
+/* Shard record (configs[3]): m_r = min J over the shard; S_r, V_r relative to m_r. */
+int oracle_shard_record(const oracle_cfg* cfg, int32_t Kr, const double* J, const float* U, const double* noise,
+                        int64_t nstride, double* rec /* [2 + T*4]: m, S, V */) {
+    double U_new_dummy[4096];
+    double* Un = cfg->T * 4 <= 4096 ? U_new_dummy : (double*)malloc(sizeof(double) * (size_t)cfg->T * 4);
+    int flag = oracle_softmin(cfg, Kr, J, U, noise, nstride, &rec[0], &rec[1], rec + 2, Un, NULL);
+    if (Un != U_new_dummy) free(Un);
+    return flag;
+}
+
+/* Combine R shard records: m = min m_r; S = sum S_r e^{-(m_r-m)/lambda}; V likewise; U_new = U + V/S. */
+int oracle_combine(const oracle_cfg* cfg, int32_t R, const double* recs, const float* U, double* U_new) {
+    const int T = cfg->T, W = 2 + T * 4;
+    double m = INFINITY;
+    for (int r = 0; r < R; ++r) if (recs[r * W] < m) m = recs[r * W];
+    if (!(m < INFINITY)) {
+        for (int i = 0; i < T * 4; ++i) U_new[i] = U[i];
+        return 1;
+    }
+    double S = 0.0;
+    double* V = (double*)calloc((size_t)T * 4, sizeof(double));
+    for (int r = 0; r < R; ++r) {
+        const double* rec = recs + (size_t)r * W;
+        if (!(rec[0] < INFINITY)) continue;
+        double f = exp(-(rec[0] - m) / cfg->lambda);
+        S += rec[1] * f;
+        for (int i = 0; i < T * 4; ++i) V[i] += rec[2 + i] * f;
+    }
+    for (int i = 0; i < T * 4; ++i) U_new[i] = (double)U[i] + V[i] / S;
+    free(V);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ full iteration */
+/* One MPPI iteration for every controller b (already-shifted nominal U). noise: [T][n_ctrl*K][4].
+ * Per-controller inputs: z [n][L], Tq [n][12], x0 [n][10], goal [n][3], U [n][T][4].
+ * Optional outputs (NULL to skip): queries [n][K][T][8], sdf [n][K][T][2], stage [n][K][T],
+ * J [n][K], Jmin/S/ess [n], V/U_new [n][T][4], flags [n]. */
+void oracle_step(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const float* Tq,
+                 const float* x0, const float* goal, const float* U, const double* noise,
+                 double* queries, double* sdf, double* stage, double* J, double* Jmin, double* S, double* ess,
+                 double* V, double* U_new, int32_t* flags) {
+    const int n = cfg->n_ctrl, K = cfg->K, T = cfg->T, L = cfg->latent_dim;
+    const int64_t nstride = (int64_t)n * K * 4;
+    double* Jl = J ? J : (double*)malloc(sizeof(double) * (size_t)n * K);
+#pragma omp parallel for schedule(dynamic, 4) collapse(2)
+    for (int bb = 0; bb < n; ++bb)
+        for (int k = 0; k < K; ++k) {
+            size_t sk = (size_t)bb * K + k;
+            Jl[sk] = oracle_rollout(cfg, W, b, z + (size_t)bb * L, Tq + (size_t)bb * 12, x0 + (size_t)bb * 10,
+                                    goal + (size_t)bb * 3, U + (size_t)bb * T * 4, noise + sk * 4, nstride, NULL,
+                                    queries ? queries + sk * T * 8 : NULL, sdf ? sdf + sk * T * 2 : NULL,
+                                    stage ? stage + sk * T : NULL);
+        }
+    double* Vt = (double*)malloc(sizeof(double) * (size_t)T * 4);
+    double* Ut = (double*)malloc(sizeof(double) * (size_t)T * 4);
+    for (int bb = 0; bb < n; ++bb) {
+        double jm, ss, es;
+        int f = oracle_softmin(cfg, K, Jl + (size_t)bb * K, U + (size_t)bb * T * 4, noise + (size_t)bb * K * 4, nstride,
+                               &jm, &ss, Vt, Ut, &es);
+        if (Jmin) Jmin[bb] = jm;
+        if (S) S[bb] = ss;
+        if (ess) ess[bb] = es;
+        if (V) memcpy(V + (size_t)bb * T * 4, Vt, sizeof(double) * (size_t)T * 4);
+        if (U_new) memcpy(U_new + (size_t)bb * T * 4, Ut, sizeof(double) * (size_t)T * 4);
+        if (flags) flags[bb] = f;
+    }
+    free(Vt);
+    free(Ut);
+    if (!J) free(Jl);
+}
+
+/* Warm-start shift ("the sequence initializes the next control cycle"):
+ * U_t <- U_{t+1}, last entry repeated. In place on [n][T][4]. */
+void oracle_shift(int32_t n, int32_t T, float* U) {
+    for (int bb = 0; bb < n; ++bb) {
+        float* u = U + (size_t)bb * T * 4;
+        for (int t = 0; t + 1 < T; ++t)
+            for (int c = 0; c < 4; ++c) u[t * 4 + c] = u[(t + 1) * 4 + c];
+    }
+}

@@ -1,0 +1,100 @@
+"""BASELINE.json configs[0..4] as plain data, plus reduced parity variants.
+
+Values come from /root/repo/BASELINE.json `configs` (cited per field below) and the readings of
+SURVEY.md §8(c) (R-numbers). Nothing here computes anything.
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+ACT_SOFTPLUS, ACT_RELU, ACT_SILU = 0, 1, 2
+MLP_FP32, MLP_BF16 = 0, 1
+
+
+@dataclass
+class MPPIConfig:
+    name: str
+    n_ctrl: int = 1              # controllers (drones) on one device (configs[4]: 1024)
+    K: int = 256                 # samples per controller (paper's M)
+    T: int = 20                  # horizon (paper's K)
+    dt: float = 0.02             # configs[0..2] dt=0.02 s; configs[3] dt=0.01 s
+    lam: float = 1.0             # temperature: configs[0] 1.0, configs[1..] 0.5
+    mass: float = 1.0            # configs[0] m = 1 kg
+    gravity: float = 9.81        # R3
+    rate_max: float = 6.0        # configs[0] body rates in +-6 rad/s
+    sigma: tuple = (2.0, 1.0, 1.0, 1.0)   # configs[0] sigma = (2 N, 1 rad/s x3)
+    w_goal: float = 1.0          # configs[0] 1.0*||p - g_c||^2
+    w_sdf: float = 50.0          # configs[0] 50*exp(-sdf/0.1)
+    sdf_scale: float = 0.1
+    sdf_exp_max: float = 80.0    # R9 overflow guard
+    w_u: float = 0.01            # configs[0] 0.01*||u||^2
+    w_guide: float = 0.0         # configs[1] -0.5*grad(sdf).v  (0 in configs[0])
+    fd_h: float = 0.1            # R12 directional forward difference step (m)
+    latent_dim: int = 32         # configs[0] 32, [1] 64, [2..3] 128, [4] 64
+    hidden: int = 64             # hidden width
+    n_hidden: int = 2            # hidden layers incl. the first (latent-conditioned) layer
+    activation: int = ACT_SOFTPLUS
+    mlp_dtype: int = MLP_FP32
+    seed: int = 0
+    steps: int = 1               # closed-loop steps the config asks for (configs[1..]: 100)
+    latent_every: int = 0        # redraw latent every N steps (configs[1]: 5)
+    per_drone_gates: bool = False  # configs[4]
+
+    @property
+    def u_lo(self):
+        return (0.0, -self.rate_max, -self.rate_max, -self.rate_max)
+
+    @property
+    def u_hi(self):
+        return (4.0 * self.mass * self.gravity, self.rate_max, self.rate_max, self.rate_max)
+
+    @property
+    def fd(self) -> bool:
+        return self.w_guide != 0.0
+
+    @property
+    def layer_dims(self):
+        """[(in, out)] for every dense layer, nn.Linear order ([out][in] weights)."""
+        dims = [(3 + self.latent_dim, self.hidden)]
+        dims += [(self.hidden, self.hidden)] * (self.n_hidden - 1)
+        dims += [(self.hidden, 1)]
+        return dims
+
+    def replace(self, **kw) -> "MPPIConfig":
+        return dataclasses.replace(self, **kw)
+
+
+CONFIGS = {
+    # configs[0]: tiny fp32 PR1 reference.
+    "c0": MPPIConfig(name="c0", K=256, T=20, dt=0.02, lam=1.0, latent_dim=32, hidden=64,
+                     n_hidden=2, activation=ACT_SOFTPLUS, mlp_dtype=MLP_FP32, w_guide=0.0),
+    # configs[1]: paper-scale single controller, 67->128->128->128->1 ReLU bf16, guidance.
+    "c1": MPPIConfig(name="c1", K=4096, T=50, dt=0.02, lam=0.5, latent_dim=64, hidden=128,
+                     n_hidden=3, activation=ACT_RELU, mlp_dtype=MLP_BF16, w_guide=0.5,
+                     steps=100, latent_every=5),
+    # configs[2]: large-sample single GPU, 131->256x4->1 SiLU bf16.
+    "c2": MPPIConfig(name="c2", K=16384, T=50, dt=0.02, lam=0.5, latent_dim=128, hidden=256,
+                     n_hidden=4, activation=ACT_SILU, mlp_dtype=MLP_BF16, w_guide=0.5,
+                     steps=100, latent_every=5),
+    # configs[3]: sharded large-K, K=131072 (global), T=100, dt=0.01, configs[2] MLP.
+    "c3": MPPIConfig(name="c3", K=131072, T=100, dt=0.01, lam=0.5, latent_dim=128, hidden=256,
+                     n_hidden=4, activation=ACT_SILU, mlp_dtype=MLP_BF16, w_guide=0.5,
+                     steps=100, latent_every=5),
+    # configs[4]: 1024 independent drones, K=1024, T=50, configs[1] MLP shared.
+    "c4": MPPIConfig(name="c4", n_ctrl=1024, K=1024, T=50, dt=0.02, lam=0.5, latent_dim=64,
+                     hidden=128, n_hidden=3, activation=ACT_RELU, mlp_dtype=MLP_BF16,
+                     w_guide=0.5, steps=100, per_drone_gates=True),
+}
+
+# Reduced parity variants: same MLP/cost/dynamics structure, sizes the oracle finishes in seconds
+# while still spanning several 128-row tiles and a ragged tail.
+CONFIGS["c1s"] = CONFIGS["c1"].replace(name="c1s", K=200, T=7, steps=1)
+CONFIGS["c2s"] = CONFIGS["c2"].replace(name="c2s", K=136, T=5, steps=1)
+CONFIGS["c3s"] = CONFIGS["c3"].replace(name="c3s", K=256, T=6, steps=1)
+CONFIGS["c4s"] = CONFIGS["c4"].replace(name="c4s", n_ctrl=6, K=64, T=4, steps=1)
+
+
+def get_config(name: str, **overrides) -> MPPIConfig:
+    cfg = CONFIGS[name]
+    return cfg.replace(**overrides) if overrides else cfg
