@@ -66,7 +66,8 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
 }
 
 /* Standard normals for global samples g0..g0+nK-1 (R24): key = seed, counter = (g, t, step_lo, step_hi);
- * u_i = ((x_i >> 8) + 0.5) * 2^-24; Box-Muller on (u0,u1) -> n0,n1 and (u2,u3) -> n2,n3.
+ * u_i = ((x_i >> 9) + 0.5) * 2^-23 in (0,1) (24 significant bits: exact in fp32 as well as fp64);
+ * Box-Muller on (u0,u1) -> n0,n1 and (u2,u3) -> n2,n3.
  * out: [T][nK][4]. */
 void oracle_noise(uint64_t seed, uint64_t step, int64_t g0, int32_t nK, int32_t T, double* out) {
     const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -78,7 +79,7 @@ void oracle_noise(uint64_t seed, uint64_t step, int64_t g0, int32_t nK, int32_t 
             uint32_t x[4];
             oracle_philox4x32_10(ctr, key, x);
             double u[4];
-            for (int j = 0; j < 4; ++j) u[j] = ((double)(x[j] >> 8) + 0.5) * (1.0 / 16777216.0);
+            for (int j = 0; j < 4; ++j) u[j] = ((double)(x[j] >> 9) + 0.5) * (1.0 / 8388608.0);
             double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
             double* o = out + ((size_t)t * nK + i) * 4;
             o[0] = r0 * cos(two_pi * u[1]);

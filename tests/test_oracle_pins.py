@@ -58,8 +58,8 @@ def test_noise_counter_layout(oracle_mod):
     other = oracle_mod.noise(seed=99, step=4, g0=0, nK=64, T=3)
     assert not np.allclose(full, other)
     x = oracle_mod.philox([5, 2, 3, 0], [99, 0])
-    u0 = ((int(x[0]) >> 8) + 0.5) / 2 ** 24
-    u1 = ((int(x[1]) >> 8) + 0.5) / 2 ** 24
+    u0 = ((int(x[0]) >> 9) + 0.5) / 2 ** 23
+    u1 = ((int(x[1]) >> 9) + 0.5) / 2 ** 23
     g = oracle_mod.noise(seed=99, step=3, g0=5, nK=1, T=3)[2, 0]
     assert g[0] == pytest.approx(math.sqrt(-2 * math.log(u0)) * math.cos(2 * math.pi * u1), rel=1e-15)
     assert g[1] == pytest.approx(math.sqrt(-2 * math.log(u0)) * math.sin(2 * math.pi * u1), rel=1e-15)
