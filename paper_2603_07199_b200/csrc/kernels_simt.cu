@@ -1,0 +1,417 @@
+// CUDA-core kernels of the MPPI hot path (sm_100a): noise + warm-start shift (K0), rollout (K1),
+// fp32 SDF-MLP (K2f, configs[0]), cost + min reduction (K3), softmin weights + update (K4),
+// shard combine, latent fold (K5). The bf16 SDF-MLP on tcgen05 tensor cores is kernel_mlp_tc.cu.
+//
+// Paper map (PAPER.md line, section/equation):
+//   K0  dU ~ N(0, Sigma)                                     PAPER.md:139 (§IV-A); generator: reading R24
+//   K1  U^m = U* + dU^m, clamp; rollout xdot = f(x,u)        PAPER.md:139, :146 (CTBR per BASELINE configs[0])
+//       query in the cached frame p_c = R p + t
+//   K2f s = g_phi(z, p_c) with the latent folded into b1'
+//   K3  J = sum of stage costs (Eq. 10 structure)
+//   K4  U* = sum_m w_m U^m, w = softmax(-J/lambda)           PAPER.md:141 (Eq. 5)
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/mppi.h"
+#include "mppi_internal.cuh"
+
+namespace mppi {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c[0], hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2], hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    }
+}
+
+__device__ __forceinline__ unsigned enc_ordered(float f) {
+    const unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float dec_ordered(unsigned e) {
+    return __uint_as_float((e & 0x80000000u) ? (e & 0x7FFFFFFFu) : ~e);
+}
+
+__device__ __forceinline__ float act_f32(int a, float x) {
+    if (a == MPPI_ACT_RELU) return fmaxf(x, 0.f);
+    if (a == MPPI_ACT_SOFTPLUS) return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x)));
+    return x / (1.f + expf(-x));  // SiLU
+}
+
+__device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
+
+// ------------------------------------------------------------------ K0: noise + warm-start shift
+// Thread i < n_ctrl*T: U_nom[b][t] = U_out[b][min(t + (step>0), T-1)] (PAPER.md:144 shift).
+// Thread i < T*n_ctrl*K (gen): Philox4x32-10(key = seed, ctr = (g, t, step_lo, step_hi)), g = global
+// sample index b*K_global + k_offset + k; u = ((x >> 9) + 0.5) 2^-23; Box-Muller -> 4 normals.
+__global__ void __launch_bounds__(256) k_noise_shift(Params p, Buffers b, int gen) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long step = *b.step;
+    if (i < (long long)p.n_ctrl * p.T) {
+        const int bb = (int)(i / p.T), t = (int)(i % p.T);
+        const int src = step > 0 ? min(t + 1, p.T - 1) : t;
+        reinterpret_cast<float4*>(b.U_nom)[i] = reinterpret_cast<const float4*>(b.U_out)[(long long)bb * p.T + src];
+    }
+    const long long NK = (long long)p.n_ctrl * p.K;
+    if (gen && i < NK * p.T) {
+        const int t = (int)(i / NK);
+        const long long j = i - (long long)t * NK;
+        const int bb = (int)(j / p.K), k = (int)(j - (long long)bb * p.K);
+        const unsigned long long g = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+        uint32_t c[4] = {(uint32_t)g, (uint32_t)t, (uint32_t)step, (uint32_t)(step >> 32)};
+        philox4x32_10(c, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+        const float s23 = 1.1920928955078125e-07f;  // 2^-23
+        const float u0 = ((float)(c[0] >> 9) + 0.5f) * s23, u1 = ((float)(c[1] >> 9) + 0.5f) * s23;
+        const float u2 = ((float)(c[2] >> 9) + 0.5f) * s23, u3 = ((float)(c[3] >> 9) + 0.5f) * s23;
+        const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+        float s0, c0, s1, c1;
+        sincospif(2.f * u1, &s0, &c0);
+        sincospif(2.f * u3, &s1, &c1);
+        b.noise[i] = make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+    }
+}
+
+void launch_noise_shift(const Params& p, const Buffers& b, bool gen, cudaStream_t s) {
+    long long n = (long long)p.n_ctrl * p.T;
+    if (gen) n = max(n, (long long)p.n_ctrl * p.K * p.T);
+    const int bs = 256;
+    k_noise_shift<<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(p, b, gen ? 1 : 0);
+}
+
+// ------------------------------------------------------------------ K1: rollout
+// One thread per (controller, sample); state in registers; time-major noise read as float4.
+__device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, float wy, float wz, float g, float* xd) {
+    const float qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+    xd[0] = x[3]; xd[1] = x[4]; xd[2] = x[5];
+    xd[3] = com * (2.f * (qx * qz + qw * qy));
+    xd[4] = com * (2.f * (qy * qz - qw * qx));
+    xd[5] = com * (1.f - 2.f * (qx * qx + qy * qy)) - g;
+    xd[6] = 0.5f * (-qx * wx - qy * wy - qz * wz);
+    xd[7] = 0.5f * (qw * wx + qy * wz - qz * wy);
+    xd[8] = 0.5f * (qw * wy + qz * wx - qx * wz);
+    xd[9] = 0.5f * (qw * wz + qx * wy - qy * wx);
+}
+
+__global__ void __launch_bounds__(128) k_rollout(Params p, Buffers b) {
+    const int bb = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) b.jmin_bits[bb] = 0xFFFFFFFFu;   // reset for K3's atomicMin
+    if (k >= p.K) return;
+    const float* x0 = b.x0 + bb * 10;
+    float x[10];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) x[i] = __ldg(x0 + i);
+    const float* Tq = b.Tq + bb * 12;
+    float R[9], tq[3], gc[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = __ldg(Tq + i);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { tq[i] = __ldg(Tq + 9 + i); gc[i] = __ldg(b.goal + bb * 3 + i); }
+    const float4* Un = reinterpret_cast<const float4*>(b.U_nom) + (long long)bb * p.T;
+    const long long NK = (long long)p.n_ctrl * p.K;
+    const long long col = (long long)bb * p.K + k;
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity;
+    float part = 0.f;
+    for (int t = 0; t < p.T; ++t) {
+        const float4 n = b.noise[(long long)t * NK + col];
+        const float4 U = Un[t];
+        const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
+        const float u1 = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
+        const float u2 = clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]);
+        const float u3 = clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]);
+        const float com = u0 / p.mass;
+        float k1[10], k2[10], k3[10], k4[10], xt[10];
+        dyn_ctbr(x, com, u1, u2, u3, g, k1);
+#pragma unroll
+        for (int i = 0; i < 10; ++i) xt[i] = x[i] + hdt * k1[i];
+        dyn_ctbr(xt, com, u1, u2, u3, g, k2);
+#pragma unroll
+        for (int i = 0; i < 10; ++i) xt[i] = x[i] + hdt * k2[i];
+        dyn_ctbr(xt, com, u1, u2, u3, g, k3);
+#pragma unroll
+        for (int i = 0; i < 10; ++i) xt[i] = x[i] + dt * k3[i];
+        dyn_ctbr(xt, com, u1, u2, u3, g, k4);
+#pragma unroll
+        for (int i = 0; i < 10; ++i) x[i] = x[i] + dt6 * (k1[i] + 2.f * k2[i] + 2.f * k3[i] + k4[i]);
+        const float qn = sqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);
+#pragma unroll
+        for (int i = 6; i < 10; ++i) x[i] = x[i] / qn;
+        // query-frame position and direction, scored at x_{t+1} (reading R7)
+        float pc[3], dv[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            pc[r] = R[3 * r] * x[0] + R[3 * r + 1] * x[1] + R[3 * r + 2] * x[2] + tq[r];
+            dv[r] = R[3 * r] * x[3] + R[3 * r + 1] * x[4] + R[3 * r + 2] * x[5];
+        }
+        const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+        const long long s = ((long long)bb * p.T + t) * p.K + k;
+        if (p.rps == 2) {
+            const float sc = nv >= 1e-6f ? p.fd_h / nv : 0.f;
+            b.rows[2 * s] = make_float4(pc[0], pc[1], pc[2], nv);
+            b.rows[2 * s + 1] = make_float4(pc[0] + sc * dv[0], pc[1] + sc * dv[1], pc[2] + sc * dv[2], 0.f);
+        } else {
+            b.rows[s] = make_float4(pc[0], pc[1], pc[2], nv);
+        }
+        const float dx = x[0] - gc[0], dy = x[1] - gc[1], dz = x[2] - gc[2];
+        part += p.w_goal * (dx * dx + dy * dy + dz * dz) + p.w_u * (u0 * u0 + u1 * u1 + u2 * u2 + u3 * u3);
+    }
+    b.partial[col] = part;
+}
+
+void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s) {
+    dim3 grid((p.K + 127) / 128, p.n_ctrl);
+    k_rollout<<<grid, 128, 0, s>>>(p, b);
+}
+
+// ------------------------------------------------------------------ K2f: fp32 SDF-MLP on CUDA cores
+// Used for MPPI_MLP_FP32 (configs[0]: 35 -> 64 -> 64 -> 1 softplus). Thread per state (states mode:
+// evaluates its rps rows and writes the SDF stage term) or per row (mppi_sdf_eval).
+template <int H>
+__device__ float mlp_row_f32(const Params& p, const float4* w1p, const float* b1f, const float* hw, const float* hb,
+                             const float* wo, float bo, float x, float y, float z) {
+    float a[H], an[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        const float4 w = w1p[j];
+        a[j] = act_f32(p.act, w.x * x + w.y * y + w.z * z + b1f[j]);
+    }
+    for (int l = 0; l < p.n_gemm; ++l) {
+        const float* W = hw + (size_t)l * H * H;
+#pragma unroll 4
+        for (int i = 0; i < H; ++i) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < H; ++j) acc = fmaf(W[i * H + j], a[j], acc);
+            an[i] = act_f32(p.act, acc + hb[l * H + i]);
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j) a[j] = an[j];
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < H; ++j) s = fmaf(wo[j], a[j], s);
+    return s + bo;
+}
+
+template <int H>
+__global__ void __launch_bounds__(128) k_mlp_simt(Params p, Buffers b, const float4* rows, long long n_items,
+                                                   int ctrl_fixed, float* sdf_out, int states_mode) {
+    extern __shared__ float smem[];
+    float* hw = smem;                                   // [n_gemm][H][H]
+    float* hb = hw + (size_t)p.n_gemm * H * H;          // [n_gemm][H]
+    float* wo = hb + p.n_gemm * H;                      // [H]
+    float4* w1p = reinterpret_cast<float4*>(wo + H);    // [H]
+    for (int i = threadIdx.x; i < p.n_gemm * H * H; i += blockDim.x) hw[i] = b.hid_w32[i];
+    for (int i = threadIdx.x; i < p.n_gemm * H; i += blockDim.x) hb[i] = b.hid_b[i];
+    for (int i = threadIdx.x; i < H; i += blockDim.x) { wo[i] = b.w_out[i]; w1p[i] = b.w1p[i]; }
+    __syncthreads();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_items) return;
+    const int rps = states_mode ? p.rps : 1;
+    const int bb = states_mode ? (int)(i / ((long long)p.T * p.K)) : ctrl_fixed;
+    const float* b1f = b.b1f + (size_t)bb * H;
+    const float bo = b.b_out[0];
+    float sv[2] = {0.f, 0.f};
+    float nv = 0.f;
+    for (int r = 0; r < rps; ++r) {
+        const float4 q = rows[i * rps + r];
+        if (r == 0) nv = q.w;
+        sv[r] = mlp_row_f32<H>(p, w1p, b1f, hw, hb, wo, bo, q.x, q.y, q.z);
+        if (sdf_out) sdf_out[i * rps + r] = sv[r];
+    }
+    if (states_mode) {
+        float term = p.w_sdf * expf(fminf(-sv[0] * p.inv_sdf_scale, p.sdf_exp_max));
+        if (rps == 2) term -= p.w_guide * nv * (sv[1] - sv[0]) * p.inv_fd_h;
+        b.terms[i] = term;
+    }
+}
+
+void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long long n_items, int ctrl_fixed,
+                     float* sdf_out, bool states_mode, cudaStream_t s) {
+    const size_t smem = sizeof(float) * ((size_t)p.n_gemm * p.H * p.H + (size_t)p.n_gemm * p.H + p.H) +
+                        sizeof(float4) * p.H;
+    const unsigned grid = (unsigned)((n_items + 127) / 128);
+    if (grid == 0) return;
+    if (p.H == 32) {
+        cudaFuncSetAttribute(k_mlp_simt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_mlp_simt<32><<<grid, 128, smem, s>>>(p, b, rows, n_items, ctrl_fixed, sdf_out, states_mode);
+    } else {
+        cudaFuncSetAttribute(k_mlp_simt<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_mlp_simt<64><<<grid, 128, smem, s>>>(p, b, rows, n_items, ctrl_fixed, sdf_out, states_mode);
+    }
+}
+
+// ------------------------------------------------------------------ K3: cost + min
+// J_k = partial_k + sum_t term[t][k]; non-finite -> +inf; J_min per controller via warp shuffles,
+// then one atomicMin per block on an order-preserving unsigned encoding (deterministic).
+__global__ void __launch_bounds__(256) k_cost_min(Params p, Buffers b) {
+    const int bb = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    float J = INFINITY;
+    if (k < p.K) {
+        float acc = b.partial[(long long)bb * p.K + k];
+        const float* tp = b.terms + (long long)bb * p.T * p.K + k;
+        for (int t = 0; t < p.T; ++t) acc += tp[(long long)t * p.K];
+        J = isfinite(acc) ? acc : INFINITY;
+        b.J[(long long)bb * p.K + k] = J;
+    }
+    unsigned e = __reduce_min_sync(0xFFFFFFFFu, enc_ordered(J));
+    __shared__ unsigned wmin[8];
+    if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned m = wmin[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
+        atomicMin(b.jmin_bits + bb, m);
+    }
+}
+
+void launch_cost_min(const Params& p, const Buffers& b, cudaStream_t s) {
+    dim3 grid((p.K + 255) / 256, p.n_ctrl);
+    k_cost_min<<<grid, 256, 0, s>>>(p, b);
+}
+
+// ------------------------------------------------------------------ K4: softmin weights + update
+// Block (t, controller): w_k = exp((J_min - J_k)/lambda); S = sum w; V_t = sum w (u_{k,t} - U*_t)
+// with u the clamped sample (reading R5); deterministic tree (shuffles, then fixed-order warps).
+// write_record: store the shard record (m_r, S_r, V_r) instead of updating (configs[3]).
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_update(Params p, Buffers b, int write_record) {
+    const int t = blockIdx.x, bb = blockIdx.y;
+    const float jmin = dec_ordered(b.jmin_bits[bb]);
+    const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+    const bool ok = isfinite(jmin);
+    float S = 0.f, S2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+    if (ok) {
+        const float* J = b.J + (long long)bb * p.K;
+        const float4* nz = b.noise + (long long)t * p.n_ctrl * p.K + (long long)bb * p.K;
+        for (int k = threadIdx.x; k < p.K; k += blockDim.x) {
+            const float Jk = J[k];
+            const float w = Jk < INFINITY ? expf((jmin - Jk) * p.inv_lambda) : 0.f;
+            const float4 n = nz[k];
+            S += w;
+            S2 += w * w;
+            v0 += w * (clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x);
+            v1 += w * (clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y);
+            v2 += w * (clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z);
+            v3 += w * (clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w);
+        }
+    }
+    __shared__ float red[8][6];
+    float vals[6] = {S, S2, v0, v1, v2, v3};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) vals[q] = warp_sum(vals[q]);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[w][q] = vals[q];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int q = 0; q < 6; ++q) {
+        float a = red[0][q];
+        for (int i = 1; i < nw; ++i) a += red[i][q];
+        vals[q] = a;
+    }
+    S = vals[0];
+    S2 = vals[1];
+    if (write_record) {
+        float* rec = b.record + (long long)bb * (2 + 4 * p.T);
+        if (t == 0) { rec[0] = jmin; rec[1] = S; }
+        rec[2 + 4 * t + 0] = vals[2];
+        rec[2 + 4 * t + 1] = vals[3];
+        rec[2 + 4 * t + 2] = vals[4];
+        rec[2 + 4 * t + 3] = vals[5];
+        return;
+    }
+    float4 Un = U;
+    if (ok && S > 0.f) {
+        Un.x = U.x + vals[2] / S;
+        Un.y = U.y + vals[3] / S;
+        Un.z = U.z + vals[4] / S;
+        Un.w = U.w + vals[5] / S;
+    }
+    reinterpret_cast<float4*>(b.U_out)[(long long)bb * p.T + t] = Un;
+    if (t == 0) {
+        float* d = b.diag + bb * 4;
+        d[0] = jmin;
+        d[1] = S;
+        d[2] = S2 > 0.f ? S * S / S2 : 0.f;
+        d[3] = ok ? 0.f : 1.f;
+        b.flags[bb] = ok ? 0 : 1;
+    }
+}
+
+void launch_update(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
+    dim3 grid(p.T, p.n_ctrl);
+    k_update<<<grid, 256, 0, s>>>(p, b, write_record ? 1 : 0);
+}
+
+// ------------------------------------------------------------------ shard combine (configs[3])
+// m = min_r m_r; S = sum_r S_r e^{-(m_r - m)/lambda}; V = sum_r V_r e^{...}; U* = U + V/S.
+// Every rank combines in rank order, so every rank gets bitwise-identical U*.
+__global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n_ctrl * p.T) return;
+    const int bb = i / p.T, t = i % p.T;
+    const int W = 2 + 4 * p.T;
+    float m = INFINITY;
+    for (int r = 0; r < R; ++r) m = fminf(m, recs[((long long)r * p.n_ctrl + bb) * W]);
+    const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+    float4 Un = U;
+    float S = 0.f, v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (isfinite(m)) {
+        for (int r = 0; r < R; ++r) {
+            const float* rec = recs + ((long long)r * p.n_ctrl + bb) * W;
+            if (!(rec[0] < INFINITY)) continue;
+            const float f = expf((m - rec[0]) * p.inv_lambda);
+            S += rec[1] * f;
+            for (int c = 0; c < 4; ++c) v[c] += rec[2 + 4 * t + c] * f;
+        }
+        if (S > 0.f) {
+            Un.x = U.x + v[0] / S; Un.y = U.y + v[1] / S; Un.z = U.z + v[2] / S; Un.w = U.w + v[3] / S;
+        }
+    }
+    reinterpret_cast<float4*>(b.U_out)[(long long)bb * p.T + t] = Un;
+    if (t == 0) {
+        float* d = b.diag + bb * 4;
+        d[0] = m;
+        d[1] = S;
+        d[2] = 0.f;   // ESS needs sum w^2 over all shards; not part of the record
+        d[3] = isfinite(m) ? 0.f : 1.f;
+        b.flags[bb] = isfinite(m) ? 0 : 1;
+    }
+}
+
+void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s) {
+    const int n = p.n_ctrl * p.T;
+    k_combine<<<(n + 127) / 128, 128, 0, s>>>(p, b, recs, R);
+}
+
+// ------------------------------------------------------------------ K5: latent fold
+// b1'[b][j] = sum_l W1[j][3+l] z_b[l] + b1[j]: the latent concat of PAPER.md:40 folded into a bias.
+__global__ void k_fold(Params p, Buffers b, int c0) {
+    const int bb = c0 + blockIdx.x;
+    for (int j = threadIdx.x; j < p.H; j += blockDim.x) {
+        float acc = b.b1[j];
+        const float* w = b.w1z + (size_t)j * p.L;
+        const float* z = b.z + (size_t)bb * p.L;
+        for (int l = 0; l < p.L; ++l) acc = fmaf(w[l], z[l], acc);
+        b.b1f[(size_t)bb * p.H + j] = acc;
+    }
+}
+
+void launch_fold(const Params& p, const Buffers& b, int c0, int count, cudaStream_t s) {
+    k_fold<<<count, 256, 0, s>>>(p, b, c0);
+}
+
+}  // namespace mppi

@@ -1,0 +1,608 @@
+// Host side of the C ABI declared in include/mppi.h: validation, workspace layout, weight packing,
+// latent fold, CUDA-graph capture of the per-step launch sequence, NCCL exchange, profiling events.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mppi.h"
+#include "mppi_internal.cuh"
+
+using namespace mppi;
+
+namespace {
+
+thread_local std::string g_err;
+
+mppi_status fail(mppi_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+constexpr int kStaging = 4;
+constexpr int kNumStages = 5;   // noise+shift, rollout, mlp, cost, update
+
+struct Layout {
+    size_t off[32];
+    size_t total;
+};
+
+enum BufId {
+    B_W1P, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
+    B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_JMIN, B_REC, B_GATH, B_DIAG, B_FLAGS, B_COUNT
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool compute_layout(const mppi_config* c, Layout* L) {
+    const size_t n = (size_t)c->n_ctrl, K = (size_t)c->K, T = (size_t)c->T, H = (size_t)c->hidden;
+    const size_t Ld = (size_t)c->latent_dim, G = (size_t)(c->n_hidden - 1);
+    const size_t rps = c->w_guide != 0.f ? 2 : 1;
+    const size_t world = (size_t)(c->world_size > 0 ? c->world_size : 1);
+    const size_t recw = 2 + 4 * T;
+    size_t sz[B_COUNT];
+    sz[B_W1P] = 16 * H;
+    sz[B_W1Z] = 4 * H * Ld;
+    sz[B_B1] = 4 * H;
+    sz[B_B1F] = 4 * n * H;
+    sz[B_HW32] = c->mlp_dtype == MPPI_MLP_FP32 ? 4 * G * H * H : 0;
+    sz[B_HWBF] = c->mlp_dtype == MPPI_MLP_BF16 ? mlp_tc_weight_bytes((int)H, (int)G) : 0;
+    sz[B_HB] = 4 * G * H;
+    sz[B_WOUT] = 4 * H;
+    sz[B_BOUT] = 16;
+    sz[B_Z] = 4 * n * Ld;
+    sz[B_TQ] = 4 * n * 12;
+    sz[B_X0] = 4 * n * 10;
+    sz[B_GOAL] = 4 * n * 3;
+    sz[B_STEP] = 16;
+    sz[B_UOUT] = 16 * n * T;
+    sz[B_UNOM] = 16 * n * T;
+    sz[B_NOISE] = 16 * T * n * K;
+    sz[B_ROWS] = 16 * n * T * K * rps + 16 * 128;   // + one tile of slack for tile-granular loads
+    sz[B_SDF] = 4 * n * T * K * rps + 4 * 128;
+    sz[B_TERMS] = 4 * n * T * K;
+    sz[B_PART] = 4 * n * K;
+    sz[B_J] = 4 * n * K;
+    sz[B_JMIN] = 4 * n;
+    sz[B_REC] = 4 * n * recw;
+    sz[B_GATH] = 4 * world * n * recw;
+    sz[B_DIAG] = 16 * n;
+    sz[B_FLAGS] = 4 * n;
+    size_t o = 0;
+    for (int i = 0; i < B_COUNT; ++i) {
+        o = align_up(o, 1024);
+        L->off[i] = o;
+        o += sz[i];
+    }
+    L->total = align_up(o, 1024);
+    return true;
+}
+
+uint16_t bf16_bits_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0x007FFFFFu) ? 0x40 : 0));
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf16_value(float f) {
+    uint32_t u = (uint32_t)bf16_bits_rne(f) << 16;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+}  // namespace
+
+struct mppi_ctx {
+    mppi_config cfg{};
+    Params p{};
+    Buffers b{};
+    Layout lay{};
+    void* ws = nullptr;
+    bool own_ws = false;
+    cudaStream_t stream = nullptr;
+    bool poisoned = false;
+    bool weights = false;
+    std::vector<char> latent_set;
+    bool use_tc = false;
+    // pinned staging ring for x0 / goal / step
+    float* h_stage[kStaging] = {};
+    cudaEvent_t stage_ev[kStaging] = {};
+    int stage_i = 0;
+    // graphs: [0] full step, [1] local (record) step
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    bool profiling = false;
+    cudaEvent_t prof_ev[kNumStages + 1] = {};
+    bool prof_valid = false;
+    ncclComm_t comm = nullptr;
+    int last_mode = -1;
+};
+
+#define CUDA_TRY(ctx, expr)                                                                             \
+    do {                                                                                                \
+        cudaError_t _e = (expr);                                                                        \
+        if (_e != cudaSuccess) {                                                                        \
+            if (ctx) (ctx)->poisoned = true;                                                            \
+            return fail(MPPI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+        }                                                                                               \
+    } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                             \
+    do {                                                                                                \
+        ncclResult_t _r = (expr);                                                                       \
+        if (_r != ncclSuccess) {                                                                        \
+            if (ctx) (ctx)->poisoned = true;                                                            \
+            return fail(MPPI_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));             \
+        }                                                                                               \
+    } while (0)
+
+static mppi_status validate(const mppi_config* c) {
+    if (!c) return fail(MPPI_ERR_INVALID, "cfg is NULL");
+    if (c->abi_version != MPPI_ABI_VERSION) return fail(MPPI_ERR_INVALID, "abi_version mismatch");
+    if (c->n_ctrl < 1 || c->K < 1 || c->T < 1) return fail(MPPI_ERR_INVALID, "n_ctrl, K, T must be >= 1");
+    if (c->K_global < c->K) return fail(MPPI_ERR_INVALID, "K_global < K");
+    if (c->k_offset < 0 || c->k_offset + c->K > c->K_global) return fail(MPPI_ERR_INVALID, "k_offset out of range");
+    if (!(c->dt > 0.f) || !(c->lambda > 0.f) || !(c->mass > 0.f)) return fail(MPPI_ERR_INVALID, "dt, lambda, mass > 0");
+    if (!(c->sdf_scale > 0.f)) return fail(MPPI_ERR_INVALID, "sdf_scale > 0");
+    if (c->w_guide != 0.f && !(c->fd_h > 0.f)) return fail(MPPI_ERR_INVALID, "fd_h > 0 with guidance");
+    for (int i = 0; i < 4; ++i)
+        if (!(c->u_lo[i] <= c->u_hi[i])) return fail(MPPI_ERR_INVALID, "u_lo > u_hi");
+    if (c->latent_dim < 0 || c->hidden < 1 || c->n_hidden < 1) return fail(MPPI_ERR_INVALID, "bad MLP dims");
+    if (c->activation < 0 || c->activation > 2) return fail(MPPI_ERR_INVALID, "bad activation");
+    if (c->noise_mode != MPPI_NOISE_DEVICE && c->noise_mode != MPPI_NOISE_EXTERNAL)
+        return fail(MPPI_ERR_INVALID, "bad noise_mode");
+    if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) return fail(MPPI_ERR_INVALID, "bad rank/world");
+    if (c->mlp_dtype == MPPI_MLP_FP32) {
+        if (c->hidden != 32 && c->hidden != 64)
+            return fail(MPPI_ERR_UNSUPPORTED, "fp32 MLP kernel supports hidden 32 or 64");
+    } else if (c->mlp_dtype == MPPI_MLP_BF16) {
+        if (!mlp_tc_supported(c->hidden, c->n_hidden - 1, c->activation))
+            return fail(MPPI_ERR_UNSUPPORTED, "bf16 tcgen05 MLP kernel: unsupported hidden width / depth");
+    } else {
+        return fail(MPPI_ERR_INVALID, "bad mlp_dtype");
+    }
+    const double rows = (double)c->n_ctrl * c->K * c->T * (c->w_guide != 0.f ? 2 : 1);
+    if (rows > 2147483647.0 * 0.5) return fail(MPPI_ERR_INVALID, "problem too large");
+    return MPPI_OK;
+}
+
+extern "C" {
+
+const char* mppi_last_error(void) { return g_err.c_str(); }
+
+size_t mppi_workspace_bytes(const mppi_config* cfg) {
+    if (validate(cfg) != MPPI_OK) return 0;
+    Layout L;
+    compute_layout(cfg, &L);
+    return L.total;
+}
+
+mppi_status mppi_get_nccl_unique_id(void* out128) {
+    if (!out128) return fail(MPPI_ERR_INVALID, "out is NULL");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(MPPI_ERR_NCCL, ncclGetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
+    return MPPI_OK;
+}
+
+mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mppi_ctx** out) {
+    if (!out) return fail(MPPI_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    mppi_status st = validate(cfg);
+    if (st != MPPI_OK) return st;
+    Layout L;
+    compute_layout(cfg, &L);
+    if (d_ws && ws_bytes < L.total) return fail(MPPI_ERR_OOM, "workspace too small");
+    mppi_ctx* ctx = new mppi_ctx();
+    ctx->cfg = *cfg;
+    ctx->lay = L;
+    ctx->stream = (cudaStream_t)cfg->stream;
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) { delete ctx; return fail(MPPI_ERR_CUDA, cudaGetErrorString(e)); }
+    if (!d_ws) {
+        e = cudaMalloc(&ctx->ws, L.total);
+        if (e != cudaSuccess) { delete ctx; return fail(MPPI_ERR_OOM, cudaGetErrorString(e)); }
+        ctx->own_ws = true;
+    } else {
+        if (((uintptr_t)d_ws) % 1024) { delete ctx; return fail(MPPI_ERR_INVALID, "workspace must be 1024-B aligned"); }
+        ctx->ws = d_ws;
+    }
+    char* base = (char*)ctx->ws;
+    Buffers& b = ctx->b;
+    b.w1p = (float4*)(base + L.off[B_W1P]);
+    b.w1z = (float*)(base + L.off[B_W1Z]);
+    b.b1 = (float*)(base + L.off[B_B1]);
+    b.b1f = (float*)(base + L.off[B_B1F]);
+    b.hid_w32 = (float*)(base + L.off[B_HW32]);
+    b.hid_wbf = (uint8_t*)(base + L.off[B_HWBF]);
+    b.hid_b = (float*)(base + L.off[B_HB]);
+    b.w_out = (float*)(base + L.off[B_WOUT]);
+    b.b_out = (float*)(base + L.off[B_BOUT]);
+    b.z = (float*)(base + L.off[B_Z]);
+    b.Tq = (float*)(base + L.off[B_TQ]);
+    b.x0 = (float*)(base + L.off[B_X0]);
+    b.goal = (float*)(base + L.off[B_GOAL]);
+    b.step = (unsigned long long*)(base + L.off[B_STEP]);
+    b.U_out = (float*)(base + L.off[B_UOUT]);
+    b.U_nom = (float*)(base + L.off[B_UNOM]);
+    b.noise = (float4*)(base + L.off[B_NOISE]);
+    b.rows = (float4*)(base + L.off[B_ROWS]);
+    b.sdf_rows = (float*)(base + L.off[B_SDF]);
+    b.terms = (float*)(base + L.off[B_TERMS]);
+    b.partial = (float*)(base + L.off[B_PART]);
+    b.J = (float*)(base + L.off[B_J]);
+    b.jmin_bits = (unsigned*)(base + L.off[B_JMIN]);
+    b.record = (float*)(base + L.off[B_REC]);
+    b.gathered = (float*)(base + L.off[B_GATH]);
+    b.diag = (float*)(base + L.off[B_DIAG]);
+    b.flags = (int*)(base + L.off[B_FLAGS]);
+
+    Params& p = ctx->p;
+    p.n_ctrl = cfg->n_ctrl; p.K = cfg->K; p.T = cfg->T;
+    p.rps = cfg->w_guide != 0.f ? 2 : 1;
+    p.H = cfg->hidden; p.L = cfg->latent_dim; p.n_gemm = cfg->n_hidden - 1; p.act = cfg->activation;
+    p.K_global = cfg->K_global; p.k_offset = cfg->k_offset;
+    p.dt = cfg->dt; p.inv_lambda = 1.f / cfg->lambda; p.mass = cfg->mass; p.gravity = cfg->gravity;
+    for (int i = 0; i < 4; ++i) { p.u_lo[i] = cfg->u_lo[i]; p.u_hi[i] = cfg->u_hi[i]; p.sigma[i] = cfg->sigma[i]; }
+    p.w_goal = cfg->w_goal; p.w_sdf = cfg->w_sdf; p.inv_sdf_scale = 1.f / cfg->sdf_scale;
+    p.sdf_exp_max = cfg->sdf_exp_max; p.w_u = cfg->w_u; p.w_guide = cfg->w_guide; p.fd_h = cfg->fd_h;
+    p.inv_fd_h = cfg->fd_h > 0.f ? 1.f / cfg->fd_h : 0.f;
+    p.seed = cfg->seed;
+    ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
+    ctx->latent_set.assign(cfg->n_ctrl, 0);
+
+    auto cleanup = [&](mppi_status s, const std::string& m) {
+        mppi_destroy(ctx);
+        return fail(s, m);
+    };
+    const size_t stage_floats = (size_t)cfg->n_ctrl * 13 + 4;
+    for (int i = 0; i < kStaging; ++i) {
+        if (cudaHostAlloc((void**)&ctx->h_stage[i], stage_floats * sizeof(float), cudaHostAllocDefault) != cudaSuccess)
+            return cleanup(MPPI_ERR_OOM, "cudaHostAlloc staging");
+        if (cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming) != cudaSuccess)
+            return cleanup(MPPI_ERR_CUDA, "cudaEventCreate");
+    }
+    for (int i = 0; i <= kNumStages; ++i)
+        if (cudaEventCreate(&ctx->prof_ev[i]) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "cudaEventCreate");
+    // zero-init the small state (U, diag, flags, step) so debug reads are defined
+    if (cudaMemsetAsync(base, 0, L.off[B_NOISE], ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "memset");
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "sync");
+    if (cfg->world_size > 1 && cfg->nccl_unique_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world_size, id, cfg->rank);
+        if (r != ncclSuccess) return cleanup(MPPI_ERR_NCCL, ncclGetErrorString(r));
+    }
+    *out = ctx;
+    return MPPI_OK;
+}
+
+mppi_status mppi_destroy(mppi_ctx* ctx) {
+    if (!ctx) return MPPI_OK;
+    for (auto& g : ctx->graph)
+        if (g) cudaGraphExecDestroy(g);
+    for (int i = 0; i < kStaging; ++i) {
+        if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+        if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+    }
+    for (auto& e : ctx->prof_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
+    delete ctx;
+    return MPPI_OK;
+}
+
+#define CHECK_CTX(ctx)                                                        \
+    do {                                                                      \
+        if (!(ctx)) return fail(MPPI_ERR_INVALID, "ctx is NULL");             \
+        if ((ctx)->poisoned) return fail(MPPI_ERR_POISONED, "context poisoned by an earlier CUDA/NCCL error"); \
+    } while (0)
+
+static void invalidate_graphs(mppi_ctx* ctx) {
+    for (auto& g : ctx->graph)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t* in_dim, const int32_t* out_dim,
+                                 const float* const* W, const float* const* bvec) {
+    CHECK_CTX(ctx);
+    const mppi_config& c = ctx->cfg;
+    const int H = c.hidden, Ld = c.latent_dim, G = c.n_hidden - 1;
+    if (n_layers != c.n_hidden + 1 || !in_dim || !out_dim || !W || !bvec)
+        return fail(MPPI_ERR_INVALID, "n_layers must be n_hidden + 1");
+    for (int l = 0; l < n_layers; ++l) {
+        const int ei = l == 0 ? 3 + Ld : H, eo = l == n_layers - 1 ? 1 : H;
+        if (in_dim[l] != ei || out_dim[l] != eo) return fail(MPPI_ERR_INVALID, "layer dims do not match the config");
+        if (!W[l] || !bvec[l]) return fail(MPPI_ERR_INVALID, "NULL weight pointer");
+    }
+    const bool bf = c.mlp_dtype == MPPI_MLP_BF16;
+    std::vector<float4> w1p(H);
+    std::vector<float> w1z((size_t)H * Ld), b1(H), hb((size_t)G * H), wo(H), bo(4, 0.f);
+    for (int j = 0; j < H; ++j) {
+        const float* r = W[0] + (size_t)j * (3 + Ld);
+        w1p[j] = make_float4(r[0], r[1], r[2], 0.f);
+        for (int l = 0; l < Ld; ++l) w1z[(size_t)j * Ld + l] = r[3 + l];
+        b1[j] = bvec[0][j];
+    }
+    std::vector<float> hw((size_t)G * H * H);
+    for (int l = 0; l < G; ++l) {
+        for (size_t i = 0; i < (size_t)H * H; ++i) hw[(size_t)l * H * H + i] = bf ? bf16_value(W[1 + l][i]) : W[1 + l][i];
+        for (int i = 0; i < H; ++i) hb[(size_t)l * H + i] = bvec[1 + l][i];
+    }
+    for (int j = 0; j < H; ++j) wo[j] = bf ? bf16_value(W[n_layers - 1][j]) : W[n_layers - 1][j];
+    bo[0] = bvec[n_layers - 1][0];
+    cudaStream_t s = ctx->stream;
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1p, w1p.data(), sizeof(float4) * H, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1z, w1z.data(), sizeof(float) * w1z.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.b1, b1.data(), sizeof(float) * H, cudaMemcpyHostToDevice));
+    if (G > 0) CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_b, hb.data(), sizeof(float) * hb.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.w_out, wo.data(), sizeof(float) * H, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.b_out, bo.data(), sizeof(float) * 4, cudaMemcpyHostToDevice));
+    if (G > 0) {
+        if (bf) {
+            std::vector<uint8_t> img(mlp_tc_weight_bytes(H, G));
+            mlp_tc_pack_weights(H, G, hw.data(), img.data());
+            CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_wbf, img.data(), img.size(), cudaMemcpyHostToDevice));
+        } else {
+            CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_w32, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    ctx->weights = true;
+    std::fill(ctx->latent_set.begin(), ctx->latent_set.end(), 0);
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q) {
+    CHECK_CTX(ctx);
+    const mppi_config& c = ctx->cfg;
+    if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "set weights before latents");
+    if (ctrl < -1 || ctrl >= c.n_ctrl || (!z && c.latent_dim > 0) || !T_q) return fail(MPPI_ERR_INVALID, "bad ctrl / NULL");
+    const int c0 = ctrl < 0 ? 0 : ctrl, cnt = ctrl < 0 ? c.n_ctrl : 1;
+    for (int i = 0; i < cnt * 12; ++i)
+        if (!std::isfinite(T_q[i])) return fail(MPPI_ERR_INVALID, "non-finite T_q");
+    cudaStream_t s = ctx->stream;
+    if (c.latent_dim > 0)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.z + (size_t)c0 * c.latent_dim, z, sizeof(float) * cnt * c.latent_dim,
+                                      cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.Tq + (size_t)c0 * 12, T_q, sizeof(float) * cnt * 12, cudaMemcpyHostToDevice, s));
+    launch_fold(ctx->p, ctx->b, c0, cnt, s);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));   // host arrays may be reused on return
+    for (int i = 0; i < cnt; ++i) ctx->latent_set[c0 + i] = 1;
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_nominal(mppi_ctx* ctx, int32_t ctrl, const float* U) {
+    CHECK_CTX(ctx);
+    const mppi_config& c = ctx->cfg;
+    if (ctrl < -1 || ctrl >= c.n_ctrl || !U) return fail(MPPI_ERR_INVALID, "bad ctrl / NULL");
+    const int c0 = ctrl < 0 ? 0 : ctrl, cnt = ctrl < 0 ? c.n_ctrl : 1;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.U_out + (size_t)c0 * c.T * 4, U, sizeof(float) * cnt * c.T * 4,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_noise(mppi_ctx* ctx, const float* d_noise) {
+    CHECK_CTX(ctx);
+    if (ctx->cfg.noise_mode != MPPI_NOISE_EXTERNAL) return fail(MPPI_ERR_INVALID, "context is not in external-noise mode");
+    if (!d_noise) return fail(MPPI_ERR_INVALID, "NULL noise");
+    const mppi_config& c = ctx->cfg;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.noise, d_noise, sizeof(float4) * (size_t)c.T * c.n_ctrl * c.K,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    return MPPI_OK;
+}
+
+static cudaError_t launch_mlp_states(mppi_ctx* ctx, cudaStream_t s) {
+    const Params& p = ctx->p;
+    const long long n_states = (long long)p.n_ctrl * p.T * p.K;
+    if (ctx->use_tc)
+        return launch_mlp_tc(p, ctx->b, ctx->b.rows, n_states * p.rps, -1, ctx->b.sdf_rows, true, s);
+    launch_mlp_simt(p, ctx->b, ctx->b.rows, n_states, -1, ctx->b.sdf_rows, true, s);
+    return cudaGetLastError();
+}
+
+// The per-step launch sequence (captured once into a CUDA graph). mode 0: full step with update
+// (and NCCL exchange + combine when a communicator exists); mode 1: local step writing the record.
+static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
+    const Params& p = ctx->p;
+    const bool prof = ctx->profiling;
+    auto mark = [&](int i) {
+        if (prof) cudaEventRecordWithFlags(ctx->prof_ev[i], s, cudaEventRecordExternal);
+    };
+    mark(0);
+    launch_noise_shift(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
+    mark(1);
+    launch_rollout(p, ctx->b, s);
+    mark(2);
+    cudaError_t e = launch_mlp_states(ctx, s);
+    if (e != cudaSuccess) return e;
+    mark(3);
+    launch_cost_min(p, ctx->b, s);
+    mark(4);
+    const bool sharded = ctx->cfg.world_size > 1;
+    if (mode == 1 || (sharded && ctx->comm)) {
+        launch_update(p, ctx->b, true, s);
+        if (mode == 0) {
+            const size_t recn = (size_t)p.n_ctrl * (2 + 4 * p.T);
+            if (ncclAllGather(ctx->b.record, ctx->b.gathered, recn, ncclFloat, ctx->comm, s) != ncclSuccess)
+                return cudaErrorUnknown;
+            launch_combine(p, ctx->b, ctx->b.gathered, ctx->cfg.world_size, s);
+        }
+    } else {
+        launch_update(p, ctx->b, false, s);
+    }
+    mark(5);
+    return cudaGetLastError();
+}
+
+static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step, bool device_inputs,
+                            int mode) {
+    CHECK_CTX(ctx);
+    if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "weights not set");
+    for (char v : ctx->latent_set)
+        if (!v) return fail(MPPI_ERR_NOT_READY, "latent not set for every controller");
+    if (!x0 || !goal) return fail(MPPI_ERR_INVALID, "NULL x0/goal");
+    if (mode == 0 && ctx->cfg.world_size > 1 && !ctx->comm)
+        return fail(MPPI_ERR_INVALID, "sharded context without NCCL: use mppi_step_local / mppi_step_finish");
+    const int n = ctx->cfg.n_ctrl;
+    cudaStream_t s = ctx->stream;
+    if (device_inputs) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, x0, sizeof(float) * n * 10, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, goal, sizeof(float) * n * 3, cudaMemcpyDeviceToDevice, s));
+        unsigned long long* hs = reinterpret_cast<unsigned long long*>(ctx->h_stage[ctx->stage_i] + (size_t)n * 13);
+        CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));
+        *hs = step;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, hs, 8, cudaMemcpyHostToDevice, s));
+    } else {
+        float* h = ctx->h_stage[ctx->stage_i];
+        CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));   // previous use of this slot done
+        std::memcpy(h, x0, sizeof(float) * n * 10);
+        std::memcpy(h + n * 10, goal, sizeof(float) * n * 3);
+        *reinterpret_cast<unsigned long long*>(h + (size_t)n * 13) = step;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, h, sizeof(float) * n * 10, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, h + n * 10, sizeof(float) * n * 3, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, h + (size_t)n * 13, 8, cudaMemcpyHostToDevice, s));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->stage_ev[ctx->stage_i], s));
+    ctx->stage_i = (ctx->stage_i + 1) % kStaging;
+    if (!ctx->graph[mode]) {
+        cudaGraph_t g;
+        CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = enqueue_step(ctx, mode, s);
+        cudaError_t e2 = cudaStreamEndCapture(s, &g);
+        if (e != cudaSuccess) {
+            if (e2 == cudaSuccess) cudaGraphDestroy(g);
+            ctx->poisoned = true;
+            return fail(MPPI_ERR_CUDA, std::string("step capture: ") + cudaGetErrorString(e));
+        }
+        CUDA_TRY(ctx, e2);
+        cudaError_t e3 = cudaGraphInstantiate(&ctx->graph[mode], g, 0);
+        cudaGraphDestroy(g);
+        CUDA_TRY(ctx, e3);
+    }
+    CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph[mode], s));
+    ctx->prof_valid = ctx->profiling;
+    ctx->last_mode = mode;
+    return MPPI_OK;
+}
+
+mppi_status mppi_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step_index) {
+    return run_step(ctx, x0, goal, step_index, false, 0);
+}
+
+mppi_status mppi_step_device(mppi_ctx* ctx, const float* d_x0, const float* d_goal, uint64_t step_index) {
+    return run_step(ctx, d_x0, d_goal, step_index, true, 0);
+}
+
+mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step_index) {
+    return run_step(ctx, x0, goal, step_index, false, 1);
+}
+
+int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 2 + 4 * ctx->cfg.T : 0; }
+
+const float* mppi_get_record_device(const mppi_ctx* ctx) { return ctx ? ctx->b.record : nullptr; }
+
+mppi_status mppi_step_finish(mppi_ctx* ctx, const float* d_records, int32_t R) {
+    CHECK_CTX(ctx);
+    if (!d_records || R < 1) return fail(MPPI_ERR_INVALID, "bad records");
+    launch_combine(ctx->p, ctx->b, d_records, R, ctx->stream);
+    CUDA_TRY(ctx, cudaGetLastError());
+    return MPPI_OK;
+}
+
+mppi_status mppi_get_controls(mppi_ctx* ctx, float* U_out, float* u0_out) {
+    CHECK_CTX(ctx);
+    if (!U_out) return fail(MPPI_ERR_INVALID, "NULL U_out");
+    const mppi_config& c = ctx->cfg;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpy(U_out, ctx->b.U_out, sizeof(float) * c.n_ctrl * c.T * 4, cudaMemcpyDeviceToHost));
+    if (u0_out)
+        for (int i = 0; i < c.n_ctrl; ++i) std::memcpy(u0_out + 4 * i, U_out + (size_t)i * c.T * 4, 16);
+    std::vector<int> flags(c.n_ctrl);
+    CUDA_TRY(ctx, cudaMemcpy(flags.data(), ctx->b.flags, sizeof(int) * c.n_ctrl, cudaMemcpyDeviceToHost));
+    for (int f : flags)
+        if (f) return fail(MPPI_ERR_NONFINITE, "every J was non-finite for some controller; its U* is unchanged");
+    return MPPI_OK;
+}
+
+mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out) {
+    CHECK_CTX(ctx);
+    if (!out) return fail(MPPI_ERR_INVALID, "NULL out");
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpy(out, ctx->b.diag, sizeof(float) * 4 * ctx->cfg.n_ctrl, cudaMemcpyDeviceToHost));
+    return MPPI_OK;
+}
+
+mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes) {
+    CHECK_CTX(ctx);
+    const Params& p = ctx->p;
+    const size_t states = (size_t)p.n_ctrl * p.T * p.K;
+    const void* src = nullptr;
+    size_t need = 0;
+    switch (what) {
+        case MPPI_DBG_QUERIES: src = ctx->b.rows; need = 16 * states * p.rps; break;
+        case MPPI_DBG_SDF: src = ctx->b.sdf_rows; need = 4 * states * p.rps; break;
+        case MPPI_DBG_COSTS: src = ctx->b.J; need = 4 * (size_t)p.n_ctrl * p.K; break;
+        case MPPI_DBG_NOISE: src = ctx->b.noise; need = 16 * states; break;
+        case MPPI_DBG_TERMS: src = ctx->b.terms; need = 4 * states; break;
+        case MPPI_DBG_PARTIAL: src = ctx->b.partial; need = 4 * (size_t)p.n_ctrl * p.K; break;
+        default: return fail(MPPI_ERR_INVALID, "bad debug id");
+    }
+    if (!host_dst || bytes < need) return fail(MPPI_ERR_INVALID, "destination too small");
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, src, need, cudaMemcpyDeviceToHost));
+    return MPPI_OK;
+}
+
+mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int64_t n, float* d_out) {
+    CHECK_CTX(ctx);
+    if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "weights not set");
+    if (ctrl < 0 || ctrl >= ctx->cfg.n_ctrl || !ctx->latent_set[ctrl]) return fail(MPPI_ERR_NOT_READY, "latent not set");
+    if (n < 0 || (n > 0 && (!d_rows || !d_out))) return fail(MPPI_ERR_INVALID, "bad rows/out");
+    if (n == 0) return MPPI_OK;
+    if (((uintptr_t)d_rows) % 16) return fail(MPPI_ERR_INVALID, "rows must be 16-B aligned");
+    cudaError_t e;
+    if (ctx->use_tc) {
+        e = launch_mlp_tc(ctx->p, ctx->b, (const float4*)d_rows, n, ctrl, d_out, false, ctx->stream);
+    } else {
+        launch_mlp_simt(ctx->p, ctx->b, (const float4*)d_rows, n, ctrl, d_out, false, ctx->stream);
+        e = cudaGetLastError();
+    }
+    CUDA_TRY(ctx, e);
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t on) {
+    CHECK_CTX(ctx);
+    if ((bool)on != ctx->profiling) {
+        ctx->profiling = on != 0;
+        invalidate_graphs(ctx);
+    }
+    return MPPI_OK;
+}
+
+mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out) {
+    CHECK_CTX(ctx);
+    if (!out || n_out < 1 || n_out > kNumStages) return fail(MPPI_ERR_INVALID, "bad out");
+    if (!ctx->prof_valid) return fail(MPPI_ERR_NOT_READY, "no profiled step yet");
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < n_out; ++i) CUDA_TRY(ctx, cudaEventElapsedTime(out + i, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+    return MPPI_OK;
+}
+
+int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
+    if (!ctx) return 0;
+    // noise+shift, rollout, mlp, cost+min, update (+ combine when sharded with NCCL)
+    return 5 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
+}
+
+}  // extern "C"

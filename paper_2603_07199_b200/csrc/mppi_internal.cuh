@@ -1,0 +1,77 @@
+// Internal declarations shared by the host orchestrator and the kernels of the B200 MPPI path.
+// Nothing here is shared with oracle/ (the CPU checker is independent by construction).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mppi {
+
+// Per-step constants, passed by value to every kernel.
+struct Params {
+    int n_ctrl, K, T;
+    int rps;              // query rows per state: 2 with FD guidance (p_c, p_c + h d), else 1
+    int H, L, n_gemm;     // hidden width, latent dim, hidden->hidden GEMM layers (n_hidden - 1)
+    int act;              // MPPI_ACT_*
+    int K_global;
+    long long k_offset;
+    float dt, inv_lambda, mass, gravity;
+    float u_lo[4], u_hi[4], sigma[4];
+    float w_goal, w_sdf, inv_sdf_scale, sdf_exp_max, w_u, w_guide, fd_h, inv_fd_h;
+    unsigned long long seed;
+};
+
+// Device buffers of one context (all inside the workspace).
+struct Buffers {
+    // MLP weights
+    float4* w1p;          // [H] (W1[j][0..2], unused) layer-1 position columns
+    float* w1z;           // [H][L] layer-1 latent columns (for the fold)
+    float* b1;            // [H]
+    float* b1f;           // [n_ctrl][H] folded bias b1' = W1z z + b1
+    float* hid_w32;       // fp32 mode: [n_gemm][H][H]
+    uint8_t* hid_wbf;     // bf16 mode: [n_gemm] swizzled UMMA B images (see kernel_mlp_tc.cu)
+    float* hid_b;         // [n_gemm][H]
+    float* w_out;         // [H] (bf16-rounded values in bf16 mode)
+    float* b_out;         // [1]
+    // controller state
+    float* z;             // [n_ctrl][L]
+    float* Tq;            // [n_ctrl][12]
+    float* x0;            // [n_ctrl][10]
+    float* goal;          // [n_ctrl][3]
+    unsigned long long* step;  // [1] step index of the current step
+    float* U_out;         // [n_ctrl][T][4] latest nominal (result of the last update)
+    float* U_nom;         // [n_ctrl][T][4] nominal used by the current step (shifted U_out)
+    float4* noise;        // [T][n_ctrl*K] standard normals
+    float4* rows;         // [n_ctrl*T*K*rps] query rows
+    float* sdf_rows;      // [n_ctrl*T*K*rps] s per row (debug)
+    float* terms;         // [n_ctrl*T*K] SDF-dependent stage cost
+    float* partial;       // [n_ctrl*K] non-SDF cost sums
+    float* J;             // [n_ctrl*K]
+    unsigned* jmin_bits;  // [n_ctrl] order-preserving encoding of min J
+    float* record;        // [n_ctrl][2 + 4T]  (m_r, S_r, V_r)
+    float* gathered;      // [world][n_ctrl][2 + 4T]
+    float* diag;          // [n_ctrl][4]
+    int* flags;           // [n_ctrl]
+};
+
+// Launchers (kernels_simt.cu)
+void launch_noise_shift(const Params& p, const Buffers& b, bool gen_noise, cudaStream_t s);
+void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s);
+void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
+                     float* sdf_out, bool states_mode, cudaStream_t s);
+void launch_cost_min(const Params& p, const Buffers& b, cudaStream_t s);
+void launch_update(const Params& p, const Buffers& b, bool write_record, cudaStream_t s);
+void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s);
+void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_count, cudaStream_t s);
+
+// tcgen05 / TMEM SDF-MLP (kernel_mlp_tc.cu)
+bool mlp_tc_supported(int H, int n_gemm, int act);
+size_t mlp_tc_weight_bytes(int H, int n_gemm);
+// Lay out bf16 weights of the n_gemm hidden layers (host, [l][H][H] fp32 nn.Linear order, already
+// bf16-representable) in the swizzled UMMA image the kernel copies to shared memory.
+void mlp_tc_pack_weights(int H, int n_gemm, const float* W, uint8_t* out);
+// rows_mode: rows are per-state query rows of the step (writes per-state SDF terms) when states_mode,
+// else arbitrary rows for mppi_sdf_eval (writes s per row only).
+cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
+                          float* sdf_out, bool states_mode, cudaStream_t s);
+
+}  // namespace mppi

@@ -1,0 +1,272 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle on identical seeded
+inputs. Tolerances (tests/gpu_helpers.py) follow north_star: 1e-5 relative on
+fp32 states/costs, 2e-2 absolute on bf16 SDF values, 1e-3 on the updated controls."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import gpu_helpers as gh
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_07199_b200 import build
+    build.build()
+    oracle.build()
+
+
+def _close(a, b, rel, abs_):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    bad = np.abs(a - b) > rel * np.abs(b) + abs_
+    return (~bad).all(), np.abs(a - b).max(initial=0.0)
+
+
+# ---------------------------------------------------------------- fp32 path (configs[0])
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_c0_step_parity(seed):
+    cfg, Ws, bs, inp, ctrl = gh.setup("c0", seed=seed)
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    Ug, u0 = ctrl.get_controls()
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    q = gh.gpu_queries_like_oracle(ctrl.debug("queries"))
+    ok, err = _close(q[..., :4], ref["queries"][..., :4], gh.REL_STATE, gh.ABS_STATE)
+    assert ok, f"queries max err {err}"
+    s = gh.gpu_sdf_like_oracle(ctrl.debug("sdf"))
+    tol_s = gh.sdf_tol(cfg, ref["sdf"])
+    assert np.all(np.abs(s - ref["sdf"]) <= tol_s), np.abs(s - ref["sdf"]).max()
+    J = ctrl.debug("costs")
+    tolJ = gh.cost_tol(cfg, ref, tol_s[..., 0])
+    assert np.all(np.abs(J - ref["J"]) <= tolJ), np.abs(J - ref["J"]).max()
+    assert np.abs(Ug - ref["U_new"]).max() <= gh.ABS_U
+    np.testing.assert_array_equal(u0, Ug[:, 0])
+
+
+# ---------------------------------------------------------------- tcgen05 bf16 MLP on given rows
+
+@pytest.mark.parametrize("name", ["c1s", "c4s"])
+def test_tc_constructed_relu_net_is_exact(name):
+    """SURVEY §8c pin: an exact ReLU network computing Eq. 2. All products are exact
+    in bf16 and all sums have <= 3 terms, so the tensor-core kernel must match the oracle's bf16
+    forward to fp32 rounding, and Eq. 2 itself within the bf16 input-rounding bound."""
+    cfg = synth.get_config(name)
+    Ws, bs = synth.constructed_gate_net(cfg)
+    cfg, _, _, inp, ctrl = gh.setup(name, weights=(Ws, bs))
+    rows = synth.make_query_rows(1000, scale=3.5, seed=11)
+    got = ctrl.sdf_eval(rows, ctrl=0).cpu().numpy()
+    oc = oracle.make_cfg(cfg)
+    ref = oracle.sdf_rows(oc, Ws, bs, inp["z"][0], rows)
+    np.testing.assert_allclose(got, ref, atol=1e-6, rtol=0)
+    eq2 = np.array([oracle.sdf_analytic(0.5, 0.375, r[:3]) for r in rows.astype(np.float64)])
+    assert np.abs(got - eq2).max() <= (0.375 + 2) * 2.0 ** (2 - 7) / 2 + 1e-6
+
+
+@pytest.mark.parametrize("name,over", [
+    ("c1s", {}),                                     # H=128, 2 GEMM layers, ReLU (configs[1] MLP)
+    ("c2s", {}),                                     # H=256, 3 GEMM layers, SiLU (configs[2] MLP)
+    ("c2s", {"n_hidden": 2}),                        # H=256, 1 GEMM layer (resident weights)
+    ("c1s", {"n_hidden": 4, "activation": 2}),       # H=128, 3 GEMM layers, SiLU
+    ("c1s", {"activation": 0}),                      # softplus on the tensor-core path
+])
+def test_tc_random_weights_rows(name, over):
+    cfg, Ws, bs, inp, ctrl = gh.setup(name, **over)
+    n = 128 * 9 + 37                                 # several tiles + ragged tail
+    rows = synth.make_query_rows(n, scale=3.0, seed=5)
+    got = ctrl.sdf_eval(rows, ctrl=0).cpu().numpy()
+    ref = oracle.sdf_rows(oracle.make_cfg(cfg), Ws, bs, inp["z"][0], rows)
+    err = np.abs(got - ref)
+    assert err.max() <= gh.ABS_SDF_BF16, err.max()
+    assert np.median(err) <= 2e-3, np.median(err)
+
+
+def test_tc_empty_and_single_row():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s")
+    assert ctrl.sdf_eval(np.zeros((0, 4), np.float32)).numel() == 0
+    rows = synth.make_query_rows(1, seed=2)
+    got = ctrl.sdf_eval(rows).cpu().numpy()
+    ref = oracle.sdf_rows(oracle.make_cfg(cfg), Ws, bs, inp["z"][0], rows)
+    assert abs(got[0] - ref[0]) <= gh.ABS_SDF_BF16
+
+
+# ---------------------------------------------------------------- full bf16 iteration
+
+def _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref):
+    Ug, _ = ctrl.get_controls(allow_nonfinite=True)
+    q = gh.gpu_queries_like_oracle(ctrl.debug("queries"))
+    ok, err = _close(q[..., :7], ref["queries"][..., :7], gh.REL_STATE, gh.ABS_STATE)
+    assert ok, f"queries max err {err}"
+    s = gh.gpu_sdf_like_oracle(ctrl.debug("sdf"))
+    assert np.abs(s - ref["sdf"]).max() <= gh.ABS_SDF_BF16
+    J = ctrl.debug("costs").astype(np.float64)
+    tolJ = gh.cost_tol(cfg, ref, gh.ABS_SDF_BF16)
+    assert np.all(np.abs(J - ref["J"]) <= tolJ)
+    for b in range(cfg.n_ctrl):
+        noise_b = np.asarray(inp["noise"])[:, b * cfg.K:(b + 1) * cfg.K]
+        # the rest is valid: the GPU update is the softmin of its own costs (K4 property)
+        prop = gh.softmin_property(cfg, inp["U"][b], noise_b, J[b])
+        assert np.abs(Ug[b] - prop).max() <= gh.ABS_U
+        # unique result: equal to the oracle's update unless the softmin winner is ambiguous
+        # under the bf16 SDF tolerance (reading R26)
+        d = np.abs(Ug[b] - ref["U_new"][b]).max()
+        if d > gh.ABS_U:
+            order = np.argsort(ref["J"][b])
+            gap = ref["J"][b][order[1]] - ref["J"][b][order[0]]
+            assert gap <= tolJ[b][order[0]] + tolJ[b][order[1]], (d, gap)
+
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s"])
+def test_bf16_step_parity(name):
+    cfg, Ws, bs, inp, ctrl = gh.setup(name)
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
+
+
+def test_multi_controller_gates():
+    """configs[4] shape: per-drone gate pose T_q, latent, goal (reduced sizes)."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c4s")
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
+
+
+def test_ragged_tiles():
+    """State count not a multiple of the 64-state tile; K not a multiple of a warp."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s", K=37, T=3)
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
+
+
+def test_single_sample_single_step():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s", K=1, T=1)
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    Ug, _ = ctrl.get_controls()
+    # K = 1: the update is the single clamped sample itself
+    np.testing.assert_allclose(Ug[0], ref["U_new"][0], atol=gh.ABS_U)
+
+
+# ---------------------------------------------------------------- noise, invariants, edge cases
+
+def test_device_noise_matches_oracle_philox():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c4s", noise_mode="device", step=3)
+    ctrl.step(inp["x0"], inp["goal"], 3)
+    ctrl.get_controls()
+    n = ctrl.debug("noise").astype(np.float64)
+    ref = oracle.noise(cfg.seed, 3, 0, cfg.n_ctrl * cfg.K, cfg.T)
+    assert np.all(np.abs(n - ref) <= 2e-6 * (1 + np.abs(ref)) * 4), np.abs(n - ref).max()
+
+
+def test_device_noise_k_offset_shards():
+    """configs[3]: rank r's noise equals the unsharded slice [r K/R, (r+1) K/R) (global counters)."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config("c3s")
+    R = 4
+    Kr = cfg.K // R
+    full = oracle.noise(cfg.seed, 0, 0, cfg.K, cfg.T)
+    for r in range(R):
+        c = Controller(cfg.replace(K=Kr), noise_mode="device", K_global=cfg.K, k_offset=r * Kr, world_size=R, rank=r)
+        Ws, bs = synth.make_weights(cfg)
+        c.set_sdf_weights(Ws, bs)
+        c.set_latent(synth.make_latents(cfg), synth.make_query_transforms(cfg))
+        c.set_nominal(synth.make_nominal(cfg))
+        c.step_local(synth.make_x0(cfg), synth.make_goals(cfg), 0)
+        n = c.debug("noise").astype(np.float64)
+        np.testing.assert_allclose(n, full[:, r * Kr:(r + 1) * Kr], rtol=1e-5, atol=1e-5)
+
+
+def test_zero_noise_keeps_nominal():
+    """north_star invariant on the GPU: sigma = 0 -> U_new == U exactly, ESS == K."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s", sigma=(0.0, 0.0, 0.0, 0.0))
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    Ug, _ = ctrl.get_controls()
+    np.testing.assert_array_equal(Ug, inp["U"])
+    d = ctrl.diagnostics()
+    assert d[0, 2] == pytest.approx(cfg.K, rel=1e-5)
+
+
+def test_hover_holds_on_gpu():
+    """Hover thrust, zero noise: every query equals the (transformed) start position exactly."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c0", sigma=(0.0, 0.0, 0.0, 0.0), gravity=float(np.float32(9.81)))
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ctrl.get_controls()
+    q = ctrl.debug("queries")
+    np.testing.assert_array_equal(q[..., :3], 0.0)
+
+
+def test_all_nonfinite_leaves_controls_unchanged():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s")
+    x0 = inp["x0"].copy()
+    x0[0, 0] = np.nan
+    ctrl.step(x0, inp["goal"], 0)
+    from paper_2603_07199_b200 import MppiError
+    with pytest.raises(MppiError) as ei:
+        ctrl.get_controls()
+    assert ei.value.status == -5
+    Ug, _ = ctrl.get_controls(allow_nonfinite=True)
+    np.testing.assert_array_equal(Ug, inp["U"])
+    assert ctrl.diagnostics()[0, 3] == 1.0
+
+
+def test_not_ready_and_invalid():
+    from paper_2603_07199_b200 import Controller, MppiError
+    cfg = synth.get_config("c1s")
+    c = Controller(cfg)
+    with pytest.raises(MppiError) as ei:
+        c.step(synth.make_x0(cfg), synth.make_goals(cfg))
+    assert ei.value.status == -4
+    with pytest.raises(MppiError):
+        c.set_sdf_weights(*synth.make_weights(cfg.replace(hidden=64)))
+    with pytest.raises(MppiError) as ei:
+        c.set_latent(synth.make_latents(cfg), synth.make_query_transforms(cfg))
+    assert ei.value.status == -4
+
+
+def test_graph_replay_is_deterministic():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c2s", noise_mode="device")
+    out = []
+    for _ in range(2):
+        ctrl.set_nominal(inp["U"])
+        ctrl.step(inp["x0"], inp["goal"], 5)
+        out.append((ctrl.get_controls()[0], ctrl.debug("costs")))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+
+
+def test_closed_loop_warm_start_c1s():
+    """configs[1] protocol (reading R19) at reduced size: 6 warm-started steps with shift, latent
+    redrawn every 5 steps, the true state advanced by the oracle's RK4 with u0 (teacher forcing:
+    the same x0 sequence goes to the GPU and to the oracle)."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s", noise_mode="device")
+    oc = oracle.make_cfg(cfg)
+    U_ref = inp["U"].copy()
+    x = inp["x0"].copy()
+    for step in range(6):
+        if step % 5 == 0 and step > 0:
+            z = synth.make_latents(cfg, frame=step // 5)
+            ctrl.set_latent(z, inp["Tq"])
+            inp["z"] = z
+        if step > 0:
+            U_ref = oracle.shift(U_ref)
+        ctrl.step(x, inp["goal"], step)
+        Ug, u0 = ctrl.get_controls()
+        noise = oracle.noise(cfg.seed, step, 0, cfg.K, cfg.T)
+        ref = oracle.step(oc, Ws, bs, inp["z"], inp["Tq"], x, inp["goal"], U_ref, noise)
+        d = np.abs(Ug - ref["U_new"]).max()
+        if d > gh.ABS_U:
+            order = np.argsort(ref["J"][0])
+            tolJ = gh.cost_tol(cfg, ref, gh.ABS_SDF_BF16)
+            assert ref["J"][0][order[1]] - ref["J"][0][order[0]] <= tolJ[0][order[0]] + tolJ[0][order[1]]
+            break   # ambiguous winner: trajectories legitimately diverge from here
+        # the oracle continues from its own update; the true state is advanced with the oracle's u0
+        U_ref = ref["U_new"].astype(np.float32)
+        x = oracle.rk4_step(x[0].astype(np.float64), ref["U_new"][0, 0], cfg.dt, cfg.mass,
+                            cfg.gravity).astype(np.float32)[None]
