@@ -1,0 +1,314 @@
+"""Benchmark of one MPPI iteration (the hot path of arxiv 2603.07199) on B200.
+
+python bench.py --gpus N --steps K --warmup W [--impl reference] [--config auto|c0..c4]
+Prints ONE JSON line (rank 0). Workload: configs[2] (K=16384, T=50, 131->256x4->1 SiLU bf16 MLP,
+FD guidance) at N=1; configs[3] (K=131072, T=100, sharded over N ranks, NCCL all-gather of the
+softmin record) for N>1. Inputs are synthetic and seeded (synth/); weights random Kaiming-uniform.
+A "step" is one full MPPI iteration: noise -> rollout -> SDF-MLP -> cost/min -> softmin update.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MPPI iteration latency (ms) and SDF-evaluated rollout-steps/sec at 1/2/4/8 B200"
+UNIT = "rollout-steps/s"
+
+
+def mlp_flops_per_row(cfg) -> int:
+    """Algorithmic flops of one SDF evaluation with the latent folded:
+    layer 1 is 3-wide (+bias), hidden GEMMs H x H, output H (2 flops per MAC)."""
+    H, G = cfg.hidden, cfg.n_hidden - 1
+    return 2 * (3 * H + G * H * H + H)
+
+
+def workload_name(cfg, world):
+    return (f"{cfg.name}: n_ctrl={cfg.n_ctrl} K={cfg.K} T={cfg.T} dt={cfg.dt} MLP {3 + cfg.latent_dim}->"
+            f"{cfg.hidden}x{cfg.n_hidden}->1 {['softplus', 'relu', 'silu'][cfg.activation]} "
+            f"{['fp32', 'bf16'][cfg.mlp_dtype]}{' + FD guidance' if cfg.fd else ''}"
+            f"{f', K sharded over {world} ranks' if world > 1 and cfg.name == 'c3' else ''}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        try:
+            lines = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        if not lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(l[1]) for l in lines]
+        mx = float(lines[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for l in lines for i in range(4) if "Active" in l[5 + i] and "Not" not in l[5 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic(cfg_name):
+    """dram bytes per MLP launch from the committed ncu --set full summary (profiles/), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")))
+        return d.get(cfg_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, seconds_target=15.0):
+    """The oracle as it stands, on this host's cores, over a bounded sample of the same workload:
+    the first k_s samples of controller 0 (same T, MLP, costs), one full oracle iteration."""
+    import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    Ws, bs = synth.make_weights(cfg)
+    oc_probe = cfg.replace(n_ctrl=1, K=8)
+    # probe the rate, then size the sample for ~seconds_target of CPU work
+    t0 = time.perf_counter()
+    _oracle_iter(oracle, oc_probe, Ws, bs)
+    dt = time.perf_counter() - t0
+    k_s = int(max(8, min(cfg.K, 8 * seconds_target / max(dt, 1e-6))))
+    k_s = max(cores, (k_s // cores) * cores)
+    sc = cfg.replace(n_ctrl=1, K=k_s)
+    t0 = time.perf_counter()
+    _oracle_iter(oracle, sc, Ws, bs)
+    dt = time.perf_counter() - t0
+    return {"value": k_s * cfg.T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"one oracle iteration over {k_s} of {cfg.K} samples x T={cfg.T} of {cfg.name} "
+                      f"(controller 0), {dt:.1f} s, OpenMP over samples"}, dt
+
+
+def _oracle_iter(oracle, cfg, Ws, bs):
+    inp = dict(z=synth.make_latents(cfg), Tq=synth.make_query_transforms(cfg), x0=synth.make_x0(cfg),
+               goal=synth.make_goals(cfg), U=synth.make_nominal(cfg))
+    noise = oracle.noise(cfg.seed, 0, 0, cfg.n_ctrl * cfg.K, cfg.T)
+    return oracle.step(oracle.make_cfg(cfg), Ws, bs, inp["z"], inp["Tq"], inp["x0"], inp["goal"], inp["U"], noise,
+                       want_queries=False)
+
+
+def pick_config(name, world):
+    if name == "auto":
+        name = "c2" if world == 1 else "c3"
+    cfg = synth.get_config(name)
+    return cfg
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cfg = pick_config(args.config, world)
+    times = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        base, dt = cpu_baseline(cfg, seconds_target=min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+        if i >= args.warmup:
+            times.append(dt)
+            info = base
+    v = info["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (bf16-emulated MLP)", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, 1) + " (oracle, bounded sample per step)"},
+            "cpu_baseline": info, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_07199_b200 import Controller, nccl_unique_id, build as b
+    b.build()
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = pick_config(args.config, world)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    # ---- shard (configs[3]: samples; configs[4]: controllers; others: replicas only)
+    K_global, k_offset, n_ctrl = cfg.K, 0, cfg.n_ctrl
+    nccl_id = None
+    sharded = world > 1 and cfg.name in ("c3",)
+    if sharded:
+        assert cfg.K % world == 0
+        K_local = cfg.K // world
+        k_offset = rank * K_local
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        K_local = cfg.K
+        if world > 1 and cfg.name == "c4":
+            n_ctrl = cfg.n_ctrl // world
+    lcfg = cfg.replace(K=K_local, n_ctrl=n_ctrl)
+    ctrl = Controller(lcfg, device=local, noise_mode="device", world_size=world if sharded else 1,
+                      rank=rank if sharded else 0, K_global=K_global, k_offset=k_offset, nccl_id=nccl_id)
+    Ws, bs = synth.make_weights(cfg)
+    ctrl.set_sdf_weights(Ws, bs)
+    Tq = synth.make_query_transforms(lcfg)
+    ctrl.set_latent(synth.make_latents(lcfg), Tq)
+    ctrl.set_nominal(synth.make_nominal(lcfg))
+    x0_h, goal_h = synth.make_x0(lcfg), synth.make_goals(lcfg)
+    dev = torch.device("cuda", local)
+    x0_d = torch.from_numpy(x0_h).to(dev)
+    goal_d = torch.from_numpy(goal_h).to(dev)
+    latents = [synth.make_latents(lcfg, frame=f) for f in range(1 + (args.warmup + args.steps) // 5)]
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    ctrl.set_profiling(True)
+
+    def one_step(i, timed):
+        if i % 5 == 0 and i > 0:
+            ctrl.set_latent(latents[i // 5], Tq)   # new depth frame every 5 steps (configs[1..3]); off the timed region
+        flush.zero_()                               # L2 flush, outside the events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctrl.step_device(x0_d, goal_d, i)
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), ctrl.kernel_times()
+
+    for i in range(args.warmup):
+        one_step(i, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms, ktimes = [], []
+    with ClockSampler(local) as clk:
+        for i in range(args.warmup, args.warmup + args.steps):
+            ms, kt = one_step(i, True)
+            step_ms.append(ms)
+            ktimes.append(kt)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    units_per_step = cfg.n_ctrl * cfg.K * cfg.T            # rollout-steps of the whole job (all ranks)
+    value = units_per_step * args.steps / (total_ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers (pinned staging H2D, D2H of U*)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctrl.set_profiling(False)
+    for i in range(3):
+        ctrl.step(x0_h, goal_h, 1000 + i)
+        ctrl.get_controls()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        ctrl.step(x0_h, goal_h, 2000 + i)
+        U, u0 = ctrl.get_controls()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = units_per_step * args.steps / e2e_s
+
+    kt = np.median(np.array(ktimes), 0)            # per-stage ms (noise, rollout, mlp, cost, update)
+    peaks, peak_src = measured_peaks()
+    rows = lcfg.n_ctrl * lcfg.K * lcfg.T * (2 if cfg.fd else 1)
+    flop = mlp_flops_per_row(cfg) * rows
+    mlp_ms = float(np.mean(np.array(ktimes)[:, 2]))
+    achieved = flop / (mlp_ms * 1e-3) / 1e12
+    traffic = ncu_traffic(cfg.name)
+    roofline = {"bound": "tensor", "kernel": "k_mlp_tc (fused SDF-MLP, tcgen05)", "achieved": achieved,
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
+                "frac_sustained": achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                "peak_source": f"{peak_src} bf16 dense (burst)", "traffic": traffic,
+                "algorithmic_flop_per_launch": flop, "flop_per_row": mlp_flops_per_row(cfg), "rows_per_launch": rows,
+                "mlp_share_of_step": mlp_ms / float(np.sum(kt)),
+                "stage_ms": {k: float(v) for k, v in zip(["noise_shift", "rollout", "sdf_mlp", "cost_min", "update"], kt)}}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if sharded or cfg.name == "c4" else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded; random Kaiming-uniform MLP weights, N(0,1) latents)",
+            "config": {"workload": workload_name(cfg, world), "n_ctrl": cfg.n_ctrl, "K": cfg.K, "T": cfg.T,
+                       "per_rank": {"n_ctrl": lcfg.n_ctrl, "K": lcfg.K},
+                       "l2": "flushed (256 MiB write) before every timed step, outside its events",
+                       "latent": "redrawn every 5 steps between timed steps (per-frame fold, off the iteration)",
+                       "parallelism": f"samples sharded x{world} + NCCL all-gather" if sharded else
+                       (f"controllers x{world}" if world > 1 else "single GPU")},
+            "latency_ms": {"mean": ms_per_step, "median": float(np.median(step_ms)),
+                           "p99": float(np.percentile(step_ms, 99))},
+            "roofline": roofline,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / args.steps,
+                    "h2d_bytes_per_step": lcfg.n_ctrl * 13 * 4 + 8, "d2h_bytes_per_step": lcfg.n_ctrl * (cfg.T * 16 + 4),
+                    "note": "mppi_step (pinned staging H2D of x0, goal) + mppi_get_controls (D2H of U*), wall clock"},
+            "gpu_launches": args.steps * ctrl.kernels_per_step(),
+            "clocks": clk.summary()}
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg)[0]
+    elif rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = None
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctrl.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -105,7 +105,9 @@ struct mppi_ctx {
     Layout lay{};
     void* ws = nullptr;
     bool own_ws = false;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // caller's stream (cfg.stream; may be the legacy default stream)
+    cudaStream_t work = nullptr;     // internal non-blocking stream the step graph is captured/launched on
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool poisoned = false;
     bool weights = false;
     std::vector<char> latent_set;
@@ -270,6 +272,10 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     }
     for (int i = 0; i <= kNumStages; ++i)
         if (cudaEventCreate(&ctx->prof_ev[i]) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "cudaEventCreate");
+    if (cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup(MPPI_ERR_CUDA, "work stream / events");
     // zero-init the small state (U, diag, flags, step) so debug reads are defined
     if (cudaMemsetAsync(base, 0, L.off[B_NOISE], ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "memset");
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "sync");
@@ -294,6 +300,9 @@ mppi_status mppi_destroy(mppi_ctx* ctx) {
     for (auto& e : ctx->prof_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->work) { cudaStreamSynchronize(ctx->work); cudaStreamDestroy(ctx->work); }
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
     delete ctx;
     return MPPI_OK;
@@ -454,7 +463,12 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     if (mode == 0 && ctx->cfg.world_size > 1 && !ctx->comm)
         return fail(MPPI_ERR_INVALID, "sharded context without NCCL: use mppi_step_local / mppi_step_finish");
     const int n = ctx->cfg.n_ctrl;
-    cudaStream_t s = ctx->stream;
+    // The graph runs on the internal stream, ordered after everything already queued on the caller's
+    // stream; the caller's stream then waits for the step (so setters, debug copies and
+    // get_controls on cfg.stream see its results).
+    cudaStream_t s = ctx->work;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_in, 0));
     if (device_inputs) {
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, x0, sizeof(float) * n * 10, cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, goal, sizeof(float) * n * 3, cudaMemcpyDeviceToDevice, s));
@@ -490,6 +504,8 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
         CUDA_TRY(ctx, e3);
     }
     CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph[mode], s));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_out, s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
     ctx->prof_valid = ctx->profiling;
     ctx->last_mode = mode;
     return MPPI_OK;

@@ -37,6 +37,29 @@ def run_oracle(cfg, Ws, bs, inp, **ov):
     return oracle.step(oc, Ws, bs, inp["z"], inp["Tq"], inp["x0"], inp["goal"], inp["U"], inp["noise"])
 
 
+# absolute floor of fp32 rollout states: v_z integrates c/m - g, a cancellation with rounding error
+# ~ulp(g)/2 per RK4 stage, i.e. <= 1e-6 m/s over a 1 s horizon
+ABS_VEL = 1e-6
+
+
+def check_queries(cfg, q_gpu, q_ref):
+    """Query rows vs the oracle. p_c and |v|: 1e-5 relative + 1e-6 absolute (north_star states).
+    FD row p_c + h v/|v|: the direction inherits the velocity's error divided by |v|, so its
+    tolerance is h * 2 (1e-5 |v| + ABS_VEL) / |v| (conditioning of the normalisation; exact 0 row
+    below |v| = 1e-6 on both sides). Returns (ok, worst excess)."""
+    a = np.asarray(q_gpu, np.float64)
+    b = np.asarray(q_ref, np.float64)
+    d = np.abs(a - b)
+    tol = REL_STATE * np.abs(b) + ABS_STATE
+    tol[..., 3] = REL_STATE * np.abs(b[..., 3]) + ABS_VEL
+    nv = np.maximum(b[..., 3:4], 1e-6)
+    dirtol = cfg.fd_h * 2 * (REL_STATE * nv + ABS_VEL) / nv
+    tol[..., 4:7] = tol[..., 0:3] + dirtol
+    m = 7 if cfg.fd else 4      # without guidance there is no FD row on the GPU
+    worst = (d[..., :m] - tol[..., :m]).max()
+    return worst <= 0, worst
+
+
 def sdf_tol(cfg, s_ref):
     if cfg.mlp_dtype == 0:
         # fp32 MLP fed fp32 query positions (rel 1e-5): |grad s| = O(1) -> same order absolute
