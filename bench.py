@@ -57,7 +57,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                          "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -159,7 +159,7 @@ def run_reference(args, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="auto")
@@ -225,13 +225,18 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1), ctrl.kernel_times()
 
-    for i in range(args.warmup):
-        one_step(i, False)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     step_ms, ktimes = [], []
+    # the sampler starts before the warm-up (nvidia-smi needs a few hundred ms to produce samples) and
+    # stops right after the timed steps
     with ClockSampler(local) as clk:
+        for i in range(args.warmup):
+            one_step(i, False)
+        time.sleep(0.3)
+        for i in range(args.warmup):
+            one_step(i, False)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         for i in range(args.warmup, args.warmup + args.steps):
             ms, kt = one_step(i, True)
             step_ms.append(ms)

@@ -1,7 +1,8 @@
 // Fused Gate-SDF MLP on 5th-generation tensor cores (sm_100a): tcgen05.mma with the activation
-// operand A and the accumulator D both in tensor memory (TMEM), weights B in shared memory staged by
-// bulk-async copies (cp.async.bulk, the TMA engine), bias + activation + bf16 pack in the epilogue,
-// the output layer and the finite-difference guidance combine fused into the last epilogue.
+// operand A and the accumulator D both in tensor memory (TMEM), the weights B resident in shared
+// memory (loaded once per persistent CTA by cp.async.bulk, i.e. the TMA engine), bias + activation +
+// bf16 pack in the epilogue, the output layer and the finite-difference guidance combine fused into
+// the last epilogue.
 //
 // Method (PAPER.md:168 "query the decoder for every predicted position", :40 latent concatenated with
 // every sampled state, folded here into the per-frame bias b1' = W1[:,3:] z + b1; Eq. 10
@@ -11,13 +12,17 @@
 //   s = w_out . a_L + b_out                                 fused into the last epilogue (fp32)
 //   term = w_sdf exp(min(-s/scale, emax)) - w_guide |v| (s(p_c + h d) - s(p_c)) / h
 //
-// Tile = 128 query rows (64 states x {p_c, p_c + h d} with guidance). One persistent CTA per SM walks
-// tiles; per tile and GEMM layer the work is split into four MMA units (N-half h, K-half c), so the
-// epilogue of N-half 0 overlaps the MMAs of N-half 1 and the next layer's K-half-0 MMAs overlap the
-// epilogue of N-half 1 (DESIGN.md §K2 for the schedule and why it keeps the tensor pipe busy).
-// TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2), A1 [3H/2, 2H) bf16 activations (2 per column).
-// Warp roles: warp 0 = MMA issuer (one thread) + TMEM allocator; warp 1 = weight producer;
-// warps 4..11 = epilogue (warp w owns TMEM lanes 32 (w%4).. and one column quarter of each N-half).
+// Work unit: a tile of 128 query rows per CTA (64 states x {p_c, p_c + h d} with guidance).
+// H = 256 (configs[2,3]) runs as CTA pairs (cluster of 2, tcgen05 cta_group::2, MMA M = 256): each
+// CTA keeps HALF of every weight matrix resident (192 KB for 3 GEMM layers) and its own 128 rows in
+// TMEM; only the pair's leader issues MMAs. H = 128 (configs[1,4]) runs one CTA per tile (cta_group::1,
+// M = 128) with all weights resident (<= 96 KB).
+// Per tile and GEMM layer the MMA work is four units (N-half h, K-half c), ordered h0c0 h0c1 h1c0 h1c1:
+// the epilogue of N-half 0 overlaps the MMAs of N-half 1, and the next layer's K-half-0 MMAs overlap
+// the epilogue of N-half 1. TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2) and
+// A1 [3H/2, 2H) bf16 activations (two per 32-bit column), alternating per layer.
+// Warp roles: warp 0 = TMEM allocator + MMA issuer (one thread of the leader CTA); warp 1 = weight
+// loader; warps 4..11 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column quarter).
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -33,60 +38,95 @@ constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kTileRows = 128;
-constexpr int kRingSlots = 4;
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// arrive on a barrier given by its shared::cluster address (possibly in the peer CTA)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+template <bool kCluster>
 __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
     uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
+    if constexpr (kCluster) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    }
     return ok != 0;
 }
 // Bounded wait: a schedule bug traps (launch error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
+template <bool kCluster = false>
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
-    while (!mbar_try_wait(a, parity)) {
+    while (!mbar_try_wait<kCluster>(bar, parity)) {
         if (++n > (1u << 26)) __trap();
     }
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+template <int CG>
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    if constexpr (CG == 1) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    } else {   // arrive on the barrier at the same offset in both CTAs of the pair
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         bar), "h"((uint16_t)3)
+                     : "memory");
+    }
 }
-// D[tmem] (+)= A[tmem] x B[smem]^T  (M=128, N from idesc, K=16; bf16 in, fp32 accumulate)
+// D[tmem] (+)= A[tmem] x B[smem]^T  (bf16 in, fp32 accumulate; M, N from idesc; K = 16)
+template <int CG>
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -109,7 +149,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart (SBO).
@@ -117,7 +156,7 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// Instruction descriptor kind::f16: D fp32, A/B bf16, both K-major, M = 128.
+// Instruction descriptor kind::f16: D fp32, A/B bf16, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -143,19 +182,33 @@ __device__ __forceinline__ float act_fn(float x) {
     }
 }
 
-// ------------------------------------------------------------------ kernel
+// ------------------------------------------------------------------ configuration
 template <int H, int G>
 struct Cfg {
+    static constexpr int CG = H == 256 ? 2 : 1;              // CTAs per MMA (cta_group)
     static constexpr int HALF = H / 2;                       // N (and K) extent of one MMA unit
-    static constexpr int UNIT_BYTES = HALF * HALF * 2;       // bf16 B block of one unit
-    static constexpr bool RESIDENT = (size_t)G * 4 * UNIT_BYTES <= 160 * 1024;
-    static constexpr int W_BYTES = RESIDENT ? G * 4 * UNIT_BYTES : kRingSlots * UNIT_BYTES;
+    static constexpr int ROWS_B = HALF / CG;                 // weight rows (N) of a unit held per CTA
+    static constexpr int UNIT_BYTES = ROWS_B * HALF * 2;     // bf16 B block of one unit in one CTA
+    static constexpr int W_BYTES = G * 4 * UNIT_BYTES;       // resident weights per CTA
     static constexpr int TMEM_COLS = 2 * H;                  // D (H) + two A regions (H/2 each)
-    static constexpr int A0 = H;                             // TMEM column of A region 0
+    static constexpr int A0 = H;
     static constexpr int QW = HALF / 2;                      // epilogue columns per warp per unit
-    static constexpr int SMEM = 1024 /*align*/ + W_BYTES + 4 * (G * H) + 4 * H + 16 * H + 4 * 2 * 2 * kTileRows +
-                                64 * 8 /*barriers*/ + 16;
+    static constexpr int MMA_M = 128 * CG;
+    // smem carve-up (offsets from the 1024-aligned base)
+    static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
+    static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
+    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [H] float4 layer-1 position cols
+    static constexpr int OFF_B1 = OFF_W1 + 16 * H;                   // [2 parity][2 slots][H] folded bias
+    static constexpr int OFF_PART = OFF_B1 + 4 * 4 * H;              // [2 parity][2 ch][128] partial dots
+    static constexpr int OFF_BAR = OFF_PART + 4 * 2 * 2 * kTileRows;
+    static constexpr int OFF_TMEM = OFF_BAR + 8 * 16;
+    static constexpr int SMEM = 1024 + OFF_TMEM + 16;
+    static_assert(SMEM <= 232448, "shared memory budget");
 };
+
+// Barrier slots (8 B each)
+enum { BAR_AREADY = 0 /*[2 regions][2 chunks]*/, BAR_DFREE = 4 /*[2]*/, BAR_MMA = 6 /*[2]*/, BAR_WLOCAL = 8,
+       BAR_WREADY = 9 };
 
 template <int H, int G, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -164,135 +217,141 @@ __global__ void __launch_bounds__(kThreads, 1)
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
              float* __restrict__ sdf_out, float* __restrict__ terms) {
     using C = Cfg<H, G>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* s_w = smem;                                             // weights (resident) or ring
-    float* s_hb = (float*)(s_w + C::W_BYTES);                        // [G][H]
-    float* s_wo = s_hb + G * H;                                      // [H]
-    float4* s_w1 = (float4*)(s_wo + H);                              // [H]
-    float* s_part = (float*)(s_w1 + H);                              // [2 parity][2 ch][128]
-    uint64_t* bars = (uint64_t*)(s_part + 2 * 2 * kTileRows);
-    uint64_t* bar_aready = bars + 0;    // [region 2][chunk 2]
-    uint64_t* bar_dfree = bars + 4;     // [2]
-    uint64_t* bar_mma = bars + 6;       // [2]
-    uint64_t* bar_full = bars + 8;      // [kRingSlots] (resident: [0] = weights loaded)
-    uint64_t* bar_empty = bars + 16;    // [kRingSlots]
-    uint32_t* s_tmem = (uint32_t*)(bars + 32);
+    constexpr int CG = C::CG;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw_u32 = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024u - (raw_u32 & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    float* s_hb = reinterpret_cast<float*>(smem + C::OFF_HB);
+    float* s_wo = reinterpret_cast<float*>(smem + C::OFF_WO);
+    float4* s_w1 = reinterpret_cast<float4*>(smem + C::OFF_W1);
+    float* s_b1 = reinterpret_cast<float*>(smem + C::OFF_B1);
+    float* s_part = reinterpret_cast<float*>(smem + C::OFF_PART);
+    const uint32_t bar0 = sbase + C::OFF_BAR;
+    auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long n_tiles = (n_rows + kTileRows - 1) / kTileRows;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const long long group = blockIdx.x / CG, n_groups = gridDim.x / CG;
+    const long long n_tiles = (n_rows + (long long)kTileRows * CG - 1) / ((long long)kTileRows * CG);
 
     // ---- setup
     for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i];
     for (int i = threadIdx.x; i < H; i += kThreads) { s_wo[i] = w_out[i]; s_w1[i] = w1p[i]; }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(bar_aready + i, kEpiWarps);
-        for (int i = 0; i < 2; ++i) { mbar_init(bar_dfree + i, kEpiWarps); mbar_init(bar_mma + i, 1); }
-        for (int i = 0; i < kRingSlots; ++i) { mbar_init(bar_full + i, 1); mbar_init(bar_empty + i, 1); }
+        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_AREADY + i), kEpiWarps * CG);
+        for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kEpiWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
+        mbar_init(bar(BAR_WLOCAL), 1);
+        mbar_init(bar(BAR_WREADY), CG);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
-                     "r"(C::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                         "r"(C::TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                         "r"(C::TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
+    // leader-CTA addresses of the scheduling barriers (the MMA issuer waits on them)
+    const uint32_t lbar0 = CG == 2 ? map_to_rank(bar0, 0) : bar0;
+    auto lbar = [&](int i) { return lbar0 + 8u * (uint32_t)i; };
 
     if (warp == 1) {
-        // ================= weight producer
-        if (lane == 0) {
-            if constexpr (C::RESIDENT) {
-                if (blockIdx.x < n_tiles) {
-                    mbar_expect_tx(bar_full, (uint32_t)C::W_BYTES);
-                    for (int u = 0; u < G * 4; ++u)
-                        bulk_g2s(s_w + (size_t)u * C::UNIT_BYTES, wimg + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
-                                 bar_full);
-                }
-            } else {
-                uint32_t it = 0;
-                for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
-                    for (int u = 0; u < G * 4; ++u, ++it) {
-                        const uint32_t slot = it % kRingSlots;
-                        if (it >= kRingSlots) mbar_wait(bar_empty + slot, ((it / kRingSlots) - 1) & 1);
-                        mbar_expect_tx(bar_full + slot, (uint32_t)C::UNIT_BYTES);
-                        bulk_g2s(s_w + (size_t)slot * C::UNIT_BYTES, wimg + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
-                                 bar_full + slot);
-                    }
-            }
+        // ================= weight loader: this CTA's half of every unit, once
+        if (lane == 0 && group < n_tiles) {
+            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)C::W_BYTES);
+            const uint8_t* src = wimg + (size_t)rank * C::W_BYTES;
+            for (int u = 0; u < G * 4; ++u)
+                bulk_g2s(sbase + (uint32_t)(u * C::UNIT_BYTES), src + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
+                         bar(BAR_WLOCAL));
+            mbar_wait(bar(BAR_WLOCAL), 0);
+            if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
+            else mbar_arrive_local(bar(BAR_WREADY));
         }
     } else if (warp == 0) {
-        // ================= MMA issuer (single thread)
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(128, C::HALF);
-            const uint32_t w_base = smem_u32(s_w);
+        // ================= MMA issuer (one thread of the leader CTA)
+        if (lane == 0 && leader && group < n_tiles) {
+            constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::HALF);
             uint32_t stage = 0;            // A stage counter (region = stage & 1)
             uint32_t d_use[2] = {0, 0};    // uses of D half h so far
-            uint32_t it = 0;               // weight ring iterator
-            bool weights_ready = false;
-            for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
+            for (long long tile = group; tile < n_tiles; tile += n_groups) {
                 for (int l = 0; l < G; ++l, ++stage) {
                     const uint32_t region = stage & 1;
                     const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
                     for (int h = 0; h < 2; ++h)
                         for (int c = 0; c < 2; ++c) {
-                            if (h == 0) {
-                                mbar_wait(bar_aready + region * 2 + c, (stage >> 1) & 1);
-                            }
+                            if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + region * 2 + c), (stage >> 1) & 1);
                             if (c == 0) {
-                                if (d_use[h] > 0) mbar_wait(bar_dfree + h, (d_use[h] - 1) & 1);
+                                if (d_use[h] > 0) mbar_wait<CG == 2>(bar(BAR_DFREE + h), (d_use[h] - 1) & 1);
                                 ++d_use[h];
                             }
-                            uint32_t b_addr;
-                            if constexpr (C::RESIDENT) {
-                                if (!weights_ready) { mbar_wait(bar_full, 0); weights_ready = true; }
-                                b_addr = w_base + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES);
-                            } else {
-                                const uint32_t slot = it % kRingSlots;
-                                mbar_wait(bar_full + slot, (it / kRingSlots) & 1);
-                                b_addr = w_base + slot * (uint32_t)C::UNIT_BYTES;
-                            }
                             tc_fence_after();
+                            const uint32_t b_addr = sbase + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES);
 #pragma unroll
                             for (int j = 0; j < C::HALF / 16; ++j) {
                                 const int kk = j * 16;
-                                const uint32_t boff = (uint32_t)((kk / 64) * (C::HALF * 128) + (kk % 64) * 2);
+                                const uint32_t boff = (uint32_t)((kk / 64) * (C::ROWS_B * 128) + (kk % 64) * 2);
                                 const uint64_t bdesc = smem_desc_sw128(b_addr + boff);
                                 const uint32_t a_t = tmem + a_col + (uint32_t)((c * C::HALF + kk) / 2);
                                 const uint32_t d_t = tmem + (uint32_t)(h * C::HALF);
-                                tc_mma_ts(d_t, a_t, bdesc, idesc, (c > 0 || j > 0) ? 1u : 0u);
+                                tc_mma_ts<CG>(d_t, a_t, bdesc, idesc, (c > 0 || j > 0) ? 1u : 0u);
                             }
-                            if constexpr (!C::RESIDENT) {
-                                tc_commit(bar_empty + (it % kRingSlots));
-                                ++it;
-                            }
-                            if (c == 1) tc_commit(bar_mma + h);
+                            if (c == 1) tc_commit<CG>(bar(BAR_MMA + h));
                         }
                 }
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ================= epilogue (8 warps)
+        // ================= epilogue (8 warps per CTA)
         const int e = warp - kEpiWarp0;
         const int g = warp & 3;            // TMEM lane quarter
         const int ch = e >> 2;             // column quarter within an N-half
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
-        uint32_t stage = 0;                // A stage produced next
+        const long long rows_per_ctrl = (long long)p.T * p.K * p.rps;
+        uint32_t stage = 0;
         uint32_t mma_cnt[2] = {0, 0};
-        long long tile = blockIdx.x;
+        int t_iter = 0;                    // tiles processed by this CTA (parity of smem double buffers)
+        auto arrive_sched = [&](int i) {   // epilogue -> MMA issuer (leader CTA)
+            if constexpr (CG == 2) mbar_arrive_cluster(lbar(i));
+            else mbar_arrive_local(bar(i));
+        };
         // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A region of `stage`
-        auto layer1 = [&](long long t1) {
-            const long long row = t1 * kTileRows + row_in_tile;
+        auto layer1 = [&](long long t1, int par) {
+            const long long row0 = t1 * (kTileRows * CG) + (long long)rank * kTileRows;
+            const long long row = row0 + row_in_tile;
+            // stage the folded bias of the (at most two) controllers of this tile in smem
+            const int bb0 = states_mode ? (int)(min(row0, n_rows - 1) / rows_per_ctrl) : ctrl_fixed;
+            float* b1s = s_b1 + par * 2 * H;
+            for (int i = threadIdx.x - kEpiWarp0 * 32; i < 2 * H; i += kEpiWarps * 32) {
+                const int bb = bb0 + i / H;
+                b1s[i] = (bb < p.n_ctrl) ? b1f[(size_t)bb * H + (i % H)] : 0.f;
+            }
+            named_bar_sync(2, kEpiWarps * 32);
             float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-            int bb = ctrl_fixed;
+            int slot = 0;
+            const float* bfg = nullptr;    // rows whose controller is beyond the two staged ones
             if (row < n_rows) {
                 q = rows[row];
-                if (states_mode) bb = (int)((row / p.rps) / ((long long)p.T * p.K));
+                if (states_mode) {
+                    const int bb = (int)(row / rows_per_ctrl);
+                    slot = bb - bb0;
+                    if (slot > 1) bfg = b1f + (size_t)bb * H;
+                }
             }
-            const float* bf = b1f + (size_t)bb * H;
+            const float* b1row = b1s + (slot > 1 ? 0 : slot) * H;
             const uint32_t region = stage & 1;
             const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
             for (int c = 0; c < 2; ++c) {
@@ -303,8 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
                         const float4 w0 = s_w1[j0 + i], w1 = s_w1[j0 + i + 1];
-                        const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, __ldg(bf + j0 + i))));
-                        const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, __ldg(bf + j0 + i + 1))));
+                        const float c0 = bfg ? __ldg(bfg + j0 + i) : b1row[j0 + i];
+                        const float c1 = bfg ? __ldg(bfg + j0 + i + 1) : b1row[j0 + i + 1];
+                        const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, c0)));
+                        const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, c1)));
                         packed[i / 2] = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
                     }
                     tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
@@ -312,25 +373,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_aready + region * 2 + c);
+                if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + c);
             }
             ++stage;
             return q.w;   // |v| of this row (meaningful on even rows in states mode)
         };
 
         float nv = 0.f;
-        if (tile < n_tiles) nv = layer1(tile);
-        for (; tile < n_tiles; tile += gridDim.x) {
-            const long long next = tile + gridDim.x;
+        long long tile = group;
+        if (tile < n_tiles) nv = layer1(tile, 0);
+        for (; tile < n_tiles; tile += n_groups, ++t_iter) {
+            const long long next = tile + n_groups;
             float sdot = 0.f;
+            float nv_next = 0.f;
+#pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
-                float nv_next = 0.f;
-                if (last && next < n_tiles) nv_next = layer1(next);   // overlaps the last layer's MMAs
+                if (last && next < n_tiles) nv_next = layer1(next, (t_iter + 1) & 1);   // overlaps the last layer's MMAs
                 const uint32_t region = stage & 1;                   // region this layer's output goes to
                 const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
+                const float* hb = s_hb + l * H;
                 for (int h = 0; h < 2; ++h) {
-                    mbar_wait(bar_mma + h, mma_cnt[h] & 1);
+                    mbar_wait(bar(BAR_MMA + h), mma_cnt[h] & 1);
                     ++mma_cnt[h];
                     tc_fence_after();
 #pragma unroll
@@ -339,21 +403,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t acc[32];
                         tmem_ld32(tmem + lane_addr + (uint32_t)j0, acc);
                         tmem_wait_ld();
-                        const float* bias = s_hb + l * H + j0;
                         if (!last) {
                             uint32_t packed[16];
 #pragma unroll
                             for (int i = 0; i < 32; i += 2) {
-                                const float x0 = __uint_as_float(acc[i]) + bias[i];
-                                const float x1 = __uint_as_float(acc[i + 1]) + bias[i + 1];
+                                const float x0 = __uint_as_float(acc[i]) + hb[j0 + i];
+                                const float x1 = __uint_as_float(acc[i + 1]) + hb[j0 + i + 1];
                                 packed[i / 2] = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
                             }
                             tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                         } else {
 #pragma unroll
                             for (int i = 0; i < 32; i += 2) {
-                                const float x0 = __uint_as_float(acc[i]) + bias[i];
-                                const float x1 = __uint_as_float(acc[i + 1]) + bias[i + 1];
+                                const float x0 = __uint_as_float(acc[i]) + hb[j0 + i];
+                                const float x1 = __uint_as_float(acc[i + 1]) + hb[j0 + i + 1];
                                 const uint32_t pk = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
                                 sdot = fmaf(__uint_as_float(pk << 16), s_wo[j0 + i], sdot);
                                 sdot = fmaf(__uint_as_float(pk & 0xFFFF0000u), s_wo[j0 + i + 1], sdot);
@@ -364,45 +427,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(bar_dfree + h);
-                        if (!last) mbar_arrive(bar_aready + region * 2 + h);
+                        arrive_sched(BAR_DFREE + h);
+                        if (!last) arrive_sched(BAR_AREADY + region * 2 + h);
                     }
                 }
                 if (!last) ++stage;
-                if (last) {
-                    // ---- output: combine the two column quarters, FD pair, write
-                    const int par = (int)(((tile - blockIdx.x) / gridDim.x) & 1);
-                    float* part = s_part + par * 2 * kTileRows;
-                    part[ch * kTileRows + row_in_tile] = sdot;
-                    named_bar_sync(1, kEpiWarps * 32);
-                    if (ch == 0) {
-                        const float s = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
-                        const long long row = tile * kTileRows + row_in_tile;
-                        if (row < n_rows && sdf_out) sdf_out[row] = s;
-                        if (states_mode) {
-                            float term;
-                            if (p.rps == 2) {
-                                const float s1 = __shfl_xor_sync(0xFFFFFFFFu, s, 1);
-                                term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                       p.w_guide * nv * (s1 - s) * p.inv_fd_h;
-                                if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
-                            } else {
-                                term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max));
-                                if (row < n_rows) terms[row] = term;
-                            }
-                        }
+            }
+            // ---- output: combine the two column quarters, FD pair, write
+            float* part = s_part + (t_iter & 1) * 2 * kTileRows;
+            part[ch * kTileRows + row_in_tile] = sdot;
+            named_bar_sync(1, kEpiWarps * 32);
+            if (ch == 0) {
+                const float s = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
+                const long long row = tile * (kTileRows * CG) + (long long)rank * kTileRows + row_in_tile;
+                if (row < n_rows && sdf_out) sdf_out[row] = s;
+                if (states_mode) {
+                    if (p.rps == 2) {
+                        const float s1 = __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+                        const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max)) -
+                                           p.w_guide * nv * (s1 - s) * p.inv_fd_h;
+                        if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
+                    } else {
+                        const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max));
+                        if (row < n_rows) terms[row] = term;
                     }
-                    nv = nv_next;
                 }
             }
+            nv = nv_next;
         }
     }
     // ---- teardown
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // the leader's MMAs wrote into this CTA's TMEM
     tc_fence_after();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+    if (warp == 0) {
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+    }
 }
 
 template <int H, int G, int ACT>
@@ -419,12 +484,24 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         attr_set = true;
     }
-    const long long tiles = (n_rows + kTileRows - 1) / kTileRows;
+    const long long tiles = (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
     if (tiles == 0) return cudaSuccess;
-    const int grid = (int)(tiles < n_sm ? tiles : n_sm);
-    k_mlp_tc<H, G, ACT><<<grid, kThreads, C::SMEM, s>>>(p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0, b.hid_wbf,
-                                                         b.hid_b, b.w_out, b.b_out, b.w1p, b.b1f, sdf_out, b.terms);
-    return cudaGetLastError();
+    const long long groups = tiles < n_sm / C::CG ? tiles : n_sm / C::CG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups * C::CG));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C::CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
+                              (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,
+                              (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms);
 }
 
 }  // namespace tc
@@ -435,28 +512,32 @@ bool mlp_tc_supported(int H, int G, int act) {
 
 size_t mlp_tc_weight_bytes(int H, int G) { return (size_t)G * H * H * 2; }
 
-// Global image = the shared-memory image: [layer][N-half h][K-half c] blocks of HALF x HALF bf16;
+// Global image = the shared-memory images of the CTA(s) of one MMA group, [rank][layer][N-half h]
+// [K-half c] blocks of ROWS_B x HALF bf16 (rank r holds rows [h HALF + r ROWS_B, +ROWS_B) of W_l);
 // inside a block, [64-wide K chunk][row n][128 B] with the 16-byte groups of row n XOR-swizzled by
 // (n % 8) (UMMA SWIZZLE_128B, K-major, 8-row atoms of 1024 B).
 void mlp_tc_pack_weights(int H, int G, const float* W, uint8_t* out) {
-    const int HALF = H / 2;
-    const size_t unit = (size_t)HALF * HALF * 2;
-    for (int l = 0; l < G; ++l)
-        for (int h = 0; h < 2; ++h)
-            for (int c = 0; c < 2; ++c) {
-                uint8_t* blk = out + (size_t)((l * 2 + h) * 2 + c) * unit;
-                for (int nn = 0; nn < HALF; ++nn)
-                    for (int kk = 0; kk < HALF; ++kk) {
-                        const float v = W[(size_t)l * H * H + (size_t)(h * HALF + nn) * H + (c * HALF + kk)];
-                        uint32_t u;
-                        std::memcpy(&u, &v, 4);   // already a bf16 value: the top 16 bits are exact
-                        const uint16_t bits = (uint16_t)(u >> 16);
-                        const int kc = kk / 64, w = kk % 64;
-                        const size_t off = (size_t)kc * HALF * 128 + (size_t)nn * 128 + (size_t)(((w / 8) ^ (nn % 8)) * 16) +
-                                           (size_t)(w % 8) * 2;
-                        std::memcpy(blk + off, &bits, 2);
-                    }
-            }
+    const int HALF = H / 2, CG = H == 256 ? 2 : 1, RB = HALF / CG;
+    const size_t unit = (size_t)RB * HALF * 2;
+    const size_t per_rank = (size_t)G * 4 * unit;
+    for (int r = 0; r < CG; ++r)
+        for (int l = 0; l < G; ++l)
+            for (int h = 0; h < 2; ++h)
+                for (int c = 0; c < 2; ++c) {
+                    uint8_t* blk = out + (size_t)r * per_rank + (size_t)((l * 2 + h) * 2 + c) * unit;
+                    for (int nn = 0; nn < RB; ++nn)
+                        for (int kk = 0; kk < HALF; ++kk) {
+                            const int n = h * HALF + r * RB + nn, k = c * HALF + kk;
+                            const float v = W[(size_t)l * H * H + (size_t)n * H + k];
+                            uint32_t u;
+                            std::memcpy(&u, &v, 4);   // already a bf16 value: the top 16 bits are exact
+                            const uint16_t bits = (uint16_t)(u >> 16);
+                            const int kc = kk / 64, w = kk % 64;
+                            const size_t off = (size_t)kc * RB * 128 + (size_t)nn * 128 +
+                                               (size_t)(((w / 8) ^ (nn % 8)) * 16) + (size_t)(w % 8) * 2;
+                            std::memcpy(blk + off, &bits, 2);
+                        }
+                }
 }
 
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
