@@ -156,6 +156,10 @@ mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out);
 /* Number of kernels this library launches per mppi_step (for the bench's gpu_launches count). */
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx);
 
+/* Debug builds only (compiled with -DMPPI_TC_TRACE): copy up to max_entries clock64 timeline records
+ * of the SDF-MLP kernel's first CTAs to host_out and reset the log; returns the count (0 in release). */
+int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries);
+
 const char* mppi_last_error(void);
 
 #ifdef __cplusplus

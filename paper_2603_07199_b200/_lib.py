@@ -22,7 +22,8 @@ EXPORTS = ["mppi_workspace_bytes", "mppi_create", "mppi_destroy", "mppi_get_nccl
            "mppi_set_sdf_weights", "mppi_set_latent", "mppi_set_nominal", "mppi_set_noise", "mppi_step",
            "mppi_step_device", "mppi_step_local", "mppi_record_size", "mppi_get_record_device",
            "mppi_step_finish", "mppi_get_controls", "mppi_get_diagnostics", "mppi_debug_copy", "mppi_sdf_eval",
-           "mppi_set_profiling", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_last_error"]
+           "mppi_set_profiling", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_debug_trace",
+           "mppi_last_error"]
 
 
 class MppiError(RuntimeError):
@@ -49,11 +50,12 @@ class MppiConfig(C.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
+def load(path: str | None = None):
     """Load libmppi_b200.so (raises if it is missing; build with paper_2603_07199_b200.build)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("MPPI_LIB", LIB_PATH)   # MPPI_LIB: e.g. the MPPI_TC_TRACE debug build
     if not os.path.exists(path):
         raise RuntimeError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(path)
@@ -81,6 +83,7 @@ def load(path: str = LIB_PATH):
         "mppi_set_profiling": ([vp, i32], i32),
         "mppi_get_kernel_times": ([vp, vp, i32], i32),
         "mppi_kernels_per_step": ([vp], i32),
+        "mppi_debug_trace": ([vp, i32], i32),
         "mppi_last_error": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():

@@ -29,25 +29,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds the debug variant libmppi_b200_trace.so (-DMPPI_TC_TRACE kernel timeline)."""
+    lib_out = LIB.replace(".so", "_trace.so") if trace else LIB
+    if not force and not trace and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib_out + f".{os.getpid()}.tmp"
     cmd = [nvcc, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", inc, "-I", os.path.join(ROOT, "include"),
-           *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp]
+           *(["-DMPPI_TC_TRACE"] if trace else []), *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc build of libmppi_b200.so failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -34,6 +34,27 @@
 namespace mppi {
 namespace tc {
 
+#ifdef MPPI_TC_TRACE
+// Debug-only timeline of the first CTAs (clock64 per SM): code = [15:14] block, [13:12] role,
+// [11:8] event, [7:6] layer, [5] half, [4] chunk, [3:0] tile & 15.
+__device__ unsigned long long g_tc_trace[1 << 16];
+__device__ unsigned int g_tc_trace_n;
+#define TC_TRACE(role, ev, l, h, c, t)                                                                       \
+    do {                                                                                                     \
+        if (blockIdx.x < 4) {                                                                                \
+            const unsigned _i = atomicAdd(&g_tc_trace_n, 1u);                                                \
+            const unsigned long long _code = ((unsigned long long)blockIdx.x << 14) | ((role) << 12) |        \
+                                             ((ev) << 8) | (((l) & 3) << 6) | (((h) & 1) << 5) |             \
+                                             (((c) & 1) << 4) | ((t) & 15);                                   \
+            if (_i < (1u << 16)) g_tc_trace[_i] = (_code << 48) | ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull); \
+        }                                                                                                    \
+    } while (0)
+#else
+#define TC_TRACE(role, ev, l, h, c, t) \
+    do {                               \
+    } while (0)
+#endif
+
 constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
@@ -292,12 +313,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
                     for (int h = 0; h < 2; ++h)
                         for (int c = 0; c < 2; ++c) {
+                            TC_TRACE(0, 0, l, h, c, tile);
                             if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + region * 2 + c), (stage >> 1) & 1);
                             if (c == 0) {
                                 if (d_use[h] > 0) mbar_wait<CG == 2>(bar(BAR_DFREE + h), (d_use[h] - 1) & 1);
                                 ++d_use[h];
                             }
                             tc_fence_after();
+                            TC_TRACE(0, 1, l, h, c, tile);
                             const uint32_t b_addr = sbase + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES);
 #pragma unroll
                             for (int j = 0; j < C::HALF / 16; ++j) {
@@ -309,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tc_mma_ts<CG>(d_t, a_t, bdesc, idesc, (c > 0 || j > 0) ? 1u : 0u);
                             }
                             if (c == 1) tc_commit<CG>(bar(BAR_MMA + h));
+                            TC_TRACE(0, 2, l, h, c, tile);
                         }
                 }
             }
@@ -330,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A region of `stage`
         auto layer1 = [&](long long t1, int par) {
+            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 6, 0, 0, 0, t1);
             const long long row0 = t1 * (kTileRows * CG) + (long long)rank * kTileRows;
             const long long row = row0 + row_in_tile;
             // stage the folded bias of the (at most two) controllers of this tile in smem
@@ -376,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + c);
             }
             ++stage;
+            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 7, 0, 0, 0, t1);
             return q.w;   // |v| of this row (meaningful on even rows in states mode)
         };
 
@@ -394,8 +420,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
                 const float* hb = s_hb + l * H;
                 for (int h = 0; h < 2; ++h) {
+                    if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 3, l, h, 0, tile);
                     mbar_wait(bar(BAR_MMA + h), mma_cnt[h] & 1);
                     ++mma_cnt[h];
+                    if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 4, l, h, 0, tile);
                     tc_fence_after();
 #pragma unroll
                     for (int q32 = 0; q32 < C::QW / 32; ++q32) {
@@ -427,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
+                        if (e == 0 || e == 7) TC_TRACE(1 + (e == 7), 5, l, h, 0, tile);
                         arrive_sched(BAR_DFREE + h);
                         if (!last) arrive_sched(BAR_AREADY + region * 2 + h);
                     }
@@ -453,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 8, 0, 0, 0, tile);
             nv = nv_next;
         }
     }
@@ -505,6 +535,24 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
 }
 
 }  // namespace tc
+
+int mlp_tc_trace_copy(unsigned long long* host, int max_entries) {
+#ifdef MPPI_TC_TRACE
+    unsigned n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, tc::g_tc_trace_n, sizeof(n));
+    if (n > (1u << 16)) n = 1u << 16;
+    if ((int)n > max_entries) n = (unsigned)max_entries;
+    cudaMemcpyFromSymbol(host, tc::g_tc_trace, sizeof(unsigned long long) * n);
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(tc::g_tc_trace_n, &zero, sizeof(zero));
+    return (int)n;
+#else
+    (void)host;
+    (void)max_entries;
+    return 0;
+#endif
+}
 
 bool mlp_tc_supported(int H, int G, int act) {
     return (H == 128 || H == 256) && G >= 1 && G <= 3 && act >= 0 && act <= 2;

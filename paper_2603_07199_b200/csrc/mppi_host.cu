@@ -615,6 +615,11 @@ mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out) {
     return MPPI_OK;
 }
 
+int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
+    if (!host_out || max_entries <= 0) return 0;
+    return mlp_tc_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
+}
+
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
     if (!ctx) return 0;
     // noise+shift, rollout, mlp, cost+min, update (+ combine when sharded with NCCL)

@@ -65,6 +65,7 @@ void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_cou
 
 // tcgen05 / TMEM SDF-MLP (kernel_mlp_tc.cu)
 bool mlp_tc_supported(int H, int n_gemm, int act);
+int mlp_tc_trace_copy(unsigned long long* host, int max_entries);   // debug builds (MPPI_TC_TRACE) only
 size_t mlp_tc_weight_bytes(int H, int n_gemm);
 // Lay out bf16 weights of the n_gemm hidden layers (host, [l][H][H] fp32 nn.Linear order, already
 // bf16-representable) in the swizzled UMMA image the kernel copies to shared memory.

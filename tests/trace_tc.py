@@ -1,0 +1,60 @@
+"""Debug timeline of the tcgen05 SDF-MLP kernel (not a test). Needs the MPPI_TC_TRACE build:
+  python paper_2603_07199_b200/build.py --trace
+  MPPI_LIB=paper_2603_07199_b200/libmppi_b200_trace.so python tests/trace_tc.py [c2|c1] [tiles_per_cta]
+Prints, for CTA 0, the cycle (clock64, relative) of every MMA-unit issue and epilogue phase."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import synth  # noqa: E402
+from tests import gpu_helpers as gh  # noqa: E402
+
+EV = {0: "mma.wait", 1: "mma.issue", 2: "mma.done_issue", 3: "epi.wait", 4: "epi.got", 5: "epi.unit_done",
+      6: "L1.start", 7: "L1.end", 8: "tile.out"}
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    tpc = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    cfg, Ws, bs, inp, ctrl = gh.setup(name + "s" if name in ("c1", "c2") else name)
+    cg = 2 if cfg.hidden == 256 else 1
+    n = 148 // cg * cg * 128 * tpc
+    rows = synth.make_query_rows(n, seed=3)
+    ctrl.sdf_eval(rows)                      # warm-up (module load)
+    lib = ctrl.lib
+    buf = np.zeros(1 << 16, np.uint64)
+    lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), 1 << 16)   # reset
+    import torch
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    ctrl.sdf_eval(rows)
+    t1.record()
+    torch.cuda.synchronize()
+    print(f"{name}: {n} rows, {t0.elapsed_time(t1) * 1e3:.1f} us (with tracing overhead)")
+    cnt = lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), 1 << 16)
+    rec = buf[:cnt]
+    code = (rec >> np.uint64(48)).astype(np.int64)
+    clk = (rec & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
+    for blk in range(2):
+        sel = ((code >> 14) & 3) == blk
+        c, k = code[sel], clk[sel]
+        order = np.argsort(k, kind="stable")
+        c, k = c[order], k[order]
+        if len(k) == 0:
+            continue
+        base = k[0]
+        print(f"--- block {blk}: {len(k)} events, span {k[-1] - base} cycles")
+        for ci, ki in zip(c, k):
+            role = ["MMA", "EPI0", "EPI7"][(ci >> 12) & 3]
+            ev = EV.get((ci >> 8) & 15, "?")
+            print(f"{ki - base:8d} {role:5s} {ev:16s} l={(ci >> 6) & 3} h={(ci >> 5) & 1} c={(ci >> 4) & 1} t={ci & 15}")
+
+
+if __name__ == "__main__":
+    main()
