@@ -35,24 +35,24 @@ namespace mppi {
 namespace tc {
 
 #ifdef MPPI_TC_TRACE
-// Debug-only timeline of the first CTAs (clock64 per SM): code = [15:14] block, [13:12] role,
-// [11:8] event, [7:6] layer, [5] half, [4] chunk, [3:0] tile & 15.
-__device__ unsigned long long g_tc_trace[1 << 16];
-__device__ unsigned int g_tc_trace_n;
-#define TC_TRACE(role, ev, l, h, c, t)                                                                       \
-    do {                                                                                                     \
-        if (blockIdx.x < 4) {                                                                                \
-            const unsigned _i = atomicAdd(&g_tc_trace_n, 1u);                                                \
-            const unsigned long long _code = ((unsigned long long)blockIdx.x << 14) | ((role) << 12) |        \
-                                             ((ev) << 8) | (((l) & 3) << 6) | (((h) & 1) << 5) |             \
-                                             (((c) & 1) << 4) | ((t) & 15);                                   \
-            if (_i < (1u << 16)) g_tc_trace[_i] = (_code << 48) | ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull); \
-        }                                                                                                    \
+// Debug-only timeline (clock64 per SM) of the first CTAs; each (block, role) appends to its own slice,
+// no atomics: code = [11:8] event, [7:6] layer, [5] half, [4] chunk, [3:0] tile & 15.
+constexpr int kTraceCap = 2048;
+__device__ unsigned long long g_tc_trace[4][3][kTraceCap];
+#define TC_TRACE(role, ev, l, h, c, t)                                                                        \
+    do {                                                                                                      \
+        if (blockIdx.x < 4 && trace_n < kTraceCap) {                                                          \
+            const unsigned long long _code = ((ev) << 8) | (((l) & 3) << 6) | (((h) & 1) << 5) |              \
+                                             (((c) & 1) << 4) | ((t) & 15);                                    \
+            g_tc_trace[blockIdx.x][role][trace_n++] = (_code << 48) | ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull); \
+        }                                                                                                     \
     } while (0)
+#define TC_TRACE_DECL int trace_n = 0
 #else
 #define TC_TRACE(role, ev, l, h, c, t) \
     do {                               \
     } while (0)
+#define TC_TRACE_DECL
 #endif
 
 constexpr int kThreads = 384;
@@ -191,15 +191,19 @@ __device__ __forceinline__ float tanh_approx(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Biases (and, for layer 1, the position weights and folded bias) are stored pre-scaled by
+// kPre<ACT> so that SiLU needs one FFMA to form h = x/2: silu(x) = x sigmoid(x) = h + h tanh(h).
 template <int ACT>
-__device__ __forceinline__ float act_fn(float x) {
+constexpr float kPre = ACT == MPPI_ACT_SILU ? 0.5f : 1.0f;
+// pre = acc * kPre + b_scaled (GEMM epilogue) or the layer-1 dot with scaled weights
+template <int ACT>
+__device__ __forceinline__ float act_pre(float pre) {
     if constexpr (ACT == MPPI_ACT_RELU) {
-        return fmaxf(x, 0.f);
+        return fmaxf(pre, 0.f);
     } else if constexpr (ACT == MPPI_ACT_SILU) {
-        const float h = 0.5f * x;             // silu(x) = x sigmoid(x) = h + h tanh(h), h = x/2
-        return fmaf(h, tanh_approx(h), h);
+        return fmaf(pre, tanh_approx(pre), pre);
     } else {
-        return fmaxf(x, 0.f) + log1pf(__expf(-fabsf(x)));
+        return fmaxf(pre, 0.f) + log1pf(__expf(-fabsf(pre)));
     }
 }
 
@@ -218,9 +222,8 @@ struct Cfg {
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
-    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [H] float4 layer-1 position cols
-    static constexpr int OFF_B1 = OFF_W1 + 16 * H;                   // [2 parity][2 slots][H] folded bias
-    static constexpr int OFF_PART = OFF_B1 + 4 * 4 * H;              // [2 parity][2 ch][128] partial dots
+    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 slots][H] float4 (W1p, b1'), scaled
+    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 parity][2 ch][128] partial dots
     static constexpr int OFF_BAR = OFF_PART + 4 * 2 * 2 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 16;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
@@ -246,21 +249,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_hb = reinterpret_cast<float*>(smem + C::OFF_HB);
     float* s_wo = reinterpret_cast<float*>(smem + C::OFF_WO);
     float4* s_w1 = reinterpret_cast<float4*>(smem + C::OFF_W1);
-    float* s_b1 = reinterpret_cast<float*>(smem + C::OFF_B1);
     float* s_part = reinterpret_cast<float*>(smem + C::OFF_PART);
     const uint32_t bar0 = sbase + C::OFF_BAR;
     auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+    constexpr float kP = kPre<ACT>;
+    TC_TRACE_DECL;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const long long group = blockIdx.x / CG, n_groups = gridDim.x / CG;
     const long long n_tiles = (n_rows + (long long)kTileRows * CG - 1) / ((long long)kTileRows * CG);
+    const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
 
     // ---- setup
-    for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i];
-    for (int i = threadIdx.x; i < H; i += kThreads) { s_wo[i] = w_out[i]; s_w1[i] = w1p[i]; }
+    for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
+    for (int i = threadIdx.x; i < H; i += kThreads) s_wo[i] = w_out[i];
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_AREADY + i), kEpiWarps * CG);
         for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kEpiWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
@@ -302,6 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 0) {
         // ================= MMA issuer (one thread of the leader CTA)
+        // Units per layer in K-chunk-major order (c0h0, c0h1, c1h0, c1h1): both K-chunk-0 units only
+        // need the first half of the previous layer's activations.
         if (lane == 0 && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::HALF);
             uint32_t stage = 0;            // A stage counter (region = stage & 1)
@@ -311,8 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int l = 0; l < G; ++l, ++stage) {
                     const uint32_t region = stage & 1;
                     const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
-                    for (int h = 0; h < 2; ++h)
-                        for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < 2; ++c)
+                        for (int h = 0; h < 2; ++h) {
                             TC_TRACE(0, 0, l, h, c, tile);
                             if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + region * 2 + c), (stage >> 1) & 1);
                             if (c == 0) {
@@ -344,39 +351,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ch = e >> 2;             // column quarter within an N-half
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
-        const long long rows_per_ctrl = (long long)p.T * p.K * p.rps;
+        const bool tracer = lane == 0 && (e == 0 || e == 7);
+        const int trole = 1 + (e == 7);
         uint32_t stage = 0;
         uint32_t mma_cnt[2] = {0, 0};
         int t_iter = 0;                    // tiles processed by this CTA (parity of smem double buffers)
+        long long staged_lo = -1;   // controllers staged_lo, staged_lo + 1 have (W1p, b1') in s_w1[0], s_w1[1]
         auto arrive_sched = [&](int i) {   // epilogue -> MMA issuer (leader CTA)
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(i));
             else mbar_arrive_local(bar(i));
         };
+        auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
+        auto load_row = [&](long long t) {
+            const long long row = tile_row0(t) + row_in_tile;
+            return row < n_rows ? __ldg(rows + row) : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
         // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A region of `stage`
-        auto layer1 = [&](long long t1, int par) {
-            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 6, 0, 0, 0, t1);
-            const long long row0 = t1 * (kTileRows * CG) + (long long)rank * kTileRows;
-            const long long row = row0 + row_in_tile;
-            // stage the folded bias of the (at most two) controllers of this tile in smem
-            const int bb0 = states_mode ? (int)(min(row0, n_rows - 1) / rows_per_ctrl) : ctrl_fixed;
-            float* b1s = s_b1 + par * 2 * H;
-            for (int i = threadIdx.x - kEpiWarp0 * 32; i < 2 * H; i += kEpiWarps * 32) {
-                const int bb = bb0 + i / H;
-                b1s[i] = (bb < p.n_ctrl) ? b1f[(size_t)bb * H + (i % H)] : 0.f;
-            }
-            named_bar_sync(2, kEpiWarps * 32);
-            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-            int slot = 0;
-            const float* bfg = nullptr;    // rows whose controller is beyond the two staged ones
-            if (row < n_rows) {
-                q = rows[row];
-                if (states_mode) {
-                    const int bb = (int)(row / rows_per_ctrl);
-                    slot = bb - bb0;
-                    if (slot > 1) bfg = b1f + (size_t)bb * H;
+        auto layer1 = [&](long long t1, const float4 q) {
+            if (tracer) TC_TRACE(trole, 6, 0, 0, 0, t1);
+            const long long row0 = tile_row0(t1);
+            const long long rlast = min(row0 + kTileRows, n_rows) - 1;
+            const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const long long hi = states_mode ? rlast / rows_per_ctrl : ctrl_fixed;
+            const bool wide = hi - lo > 1;            // > 2 controllers in one tile (tiny K*T only)
+            if (lo != staged_lo) {   // s_w1 holds controllers lo and lo + 1
+                // uniform across the epilogue warps; the previous tile's layer 1 is behind bar 1
+                for (int i = threadIdx.x - kEpiWarp0 * 32; i < 2 * H; i += kEpiWarps * 32) {
+                    const long long bb = lo + i / H;
+                    const int j = i % H;
+                    const float4 w = w1p[j];
+                    const float bv = bb < p.n_ctrl ? b1f[(size_t)bb * H + j] : 0.f;
+                    s_w1[i] = make_float4(w.x * kP, w.y * kP, w.z * kP, bv * kP);
                 }
+                staged_lo = lo;
+                named_bar_sync(2, kEpiWarps * 32);
             }
-            const float* b1row = b1s + (slot > 1 ? 0 : slot) * H;
+            const long long row = row0 + row_in_tile;
+            const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const int slot = (int)min(bb - lo, 1ll);
+            const float4* wrow = s_w1 + slot * H;
+            const float* bfar = (wide && bb - lo > 1) ? b1f + (size_t)bb * H : nullptr;
             const uint32_t region = stage & 1;
             const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
             for (int c = 0; c < 2; ++c) {
@@ -384,14 +398,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q32 = 0; q32 < C::QW / 32; ++q32) {
                     const int j0 = c * C::HALF + ch * C::QW + q32 * 32;
                     uint32_t packed[16];
+                    if (!__any_sync(0xFFFFFFFFu, bfar != nullptr)) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float4 w0 = s_w1[j0 + i], w1 = s_w1[j0 + i + 1];
-                        const float c0 = bfg ? __ldg(bfg + j0 + i) : b1row[j0 + i];
-                        const float c1 = bfg ? __ldg(bfg + j0 + i + 1) : b1row[j0 + i + 1];
-                        const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, c0)));
-                        const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, c1)));
-                        packed[i / 2] = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
+                        for (int i = 0; i < 32; i += 2) {
+                            const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
+                            const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, w0.w)));
+                            const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
+                            packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                        }
+                    } else {   // rare: rows of a third controller in this tile
+#pragma unroll 1
+                        for (int i = 0; i < 32; i += 2) {
+                            const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
+                            const float b0 = bfar ? __ldg(bfar + j0 + i) * kP : w0.w;
+                            const float b1 = bfar ? __ldg(bfar + j0 + i + 1) * kP : w1.w;
+                            const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, b0)));
+                            const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, b1)));
+                            packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                        }
                     }
                     tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                 }
@@ -401,64 +425,80 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + c);
             }
             ++stage;
-            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 7, 0, 0, 0, t1);
-            return q.w;   // |v| of this row (meaningful on even rows in states mode)
+            if (tracer) TC_TRACE(trole, 7, 0, 0, 0, t1);
         };
 
-        float nv = 0.f;
         long long tile = group;
-        if (tile < n_tiles) nv = layer1(tile, 0);
+        float4 q_cur = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tile < n_tiles) {
+            q_cur = load_row(tile);
+            layer1(tile, q_cur);
+        }
         for (; tile < n_tiles; tile += n_groups, ++t_iter) {
             const long long next = tile + n_groups;
+            const float4 q_next = next < n_tiles ? load_row(next) : make_float4(0.f, 0.f, 0.f, 0.f);  // prefetch
             float sdot = 0.f;
-            float nv_next = 0.f;
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
-                if (last && next < n_tiles) nv_next = layer1(next, (t_iter + 1) & 1);   // overlaps the last layer's MMAs
+                if (last && next < n_tiles) layer1(next, q_next);   // overlaps the last layer's MMAs
                 const uint32_t region = stage & 1;                   // region this layer's output goes to
                 const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
                 const float* hb = s_hb + l * H;
                 for (int h = 0; h < 2; ++h) {
-                    if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 3, l, h, 0, tile);
+                    if (tracer) TC_TRACE(trole, 3, l, h, 0, tile);
                     mbar_wait(bar(BAR_MMA + h), mma_cnt[h] & 1);
                     ++mma_cnt[h];
-                    if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 4, l, h, 0, tile);
                     tc_fence_after();
+                    if (tracer) TC_TRACE(trole, 4, l, h, 0, tile);
+                    // read all of this warp's accumulator columns of N-half h, then release D[h] at once
+                    uint32_t acc[C::QW / 32][32];
+#pragma unroll
+                    for (int q32 = 0; q32 < C::QW / 32; ++q32)
+                        tmem_ld32(tmem + lane_addr + (uint32_t)(h * C::HALF + ch * C::QW + q32 * 32), acc[q32]);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive_sched(BAR_DFREE + h);
 #pragma unroll
                     for (int q32 = 0; q32 < C::QW / 32; ++q32) {
                         const int j0 = h * C::HALF + ch * C::QW + q32 * 32;
-                        uint32_t acc[32];
-                        tmem_ld32(tmem + lane_addr + (uint32_t)j0, acc);
-                        tmem_wait_ld();
                         if (!last) {
                             uint32_t packed[16];
 #pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float x0 = __uint_as_float(acc[i]) + hb[j0 + i];
-                                const float x1 = __uint_as_float(acc[i + 1]) + hb[j0 + i + 1];
-                                packed[i / 2] = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
+                            for (int i = 0; i < 32; i += 4) {
+                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
+                                const float x0 = fmaf(__uint_as_float(acc[q32][i]), kP, bv.x);
+                                const float x1 = fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y);
+                                const float x2 = fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z);
+                                const float x3 = fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w);
+                                packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                                packed[i / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
                             }
                             tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                         } else {
 #pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float x0 = __uint_as_float(acc[i]) + hb[j0 + i];
-                                const float x1 = __uint_as_float(acc[i + 1]) + hb[j0 + i + 1];
-                                const uint32_t pk = pack_bf16x2(act_fn<ACT>(x0), act_fn<ACT>(x1));
-                                sdot = fmaf(__uint_as_float(pk << 16), s_wo[j0 + i], sdot);
-                                sdot = fmaf(__uint_as_float(pk & 0xFFFF0000u), s_wo[j0 + i + 1], sdot);
+                            for (int i = 0; i < 32; i += 4) {
+                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
+                                const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
+                                const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i]), kP, bv.x)),
+                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y)));
+                                const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z)),
+                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w)));
+                                sdot = fmaf(__uint_as_float(p0 << 16), wv.x, sdot);
+                                sdot = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot);
+                                sdot = fmaf(__uint_as_float(p1 << 16), wv.z, sdot);
+                                sdot = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot);
                             }
                         }
                     }
-                    if (!last) tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (e == 0 || e == 7) TC_TRACE(1 + (e == 7), 5, l, h, 0, tile);
-                        arrive_sched(BAR_DFREE + h);
-                        if (!last) arrive_sched(BAR_AREADY + region * 2 + h);
+                    if (!last) {
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + h);
                     }
+                    if (tracer) TC_TRACE(trole, 5, l, h, 0, tile);
                 }
                 if (!last) ++stage;
             }
@@ -468,13 +508,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1, kEpiWarps * 32);
             if (ch == 0) {
                 const float s = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
-                const long long row = tile * (kTileRows * CG) + (long long)rank * kTileRows + row_in_tile;
+                const long long row = tile_row0(tile) + row_in_tile;
                 if (row < n_rows && sdf_out) sdf_out[row] = s;
                 if (states_mode) {
                     if (p.rps == 2) {
                         const float s1 = __shfl_xor_sync(0xFFFFFFFFu, s, 1);
                         const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                           p.w_guide * nv * (s1 - s) * p.inv_fd_h;
+                                           p.w_guide * q_cur.w * (s1 - s) * p.inv_fd_h;
                         if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
                     } else {
                         const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max));
@@ -482,8 +522,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (lane == 0 && (e == 0 || e == 7)) TC_TRACE(1 + (e == 7), 8, 0, 0, 0, tile);
-            nv = nv_next;
+            if (tracer) TC_TRACE(trole, 8, 0, 0, 0, tile);
+            q_cur = q_next;
         }
     }
     // ---- teardown
@@ -538,15 +578,13 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
 
 int mlp_tc_trace_copy(unsigned long long* host, int max_entries) {
 #ifdef MPPI_TC_TRACE
-    unsigned n = 0;
+    const int n = 4 * 3 * tc::kTraceCap;
+    if (max_entries < n) return 0;
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(&n, tc::g_tc_trace_n, sizeof(n));
-    if (n > (1u << 16)) n = 1u << 16;
-    if ((int)n > max_entries) n = (unsigned)max_entries;
     cudaMemcpyFromSymbol(host, tc::g_tc_trace, sizeof(unsigned long long) * n);
-    const unsigned zero = 0;
-    cudaMemcpyToSymbol(tc::g_tc_trace_n, &zero, sizeof(zero));
-    return (int)n;
+    static unsigned long long zeros[4 * 3 * tc::kTraceCap];
+    cudaMemcpyToSymbol(tc::g_tc_trace, zeros, sizeof(zeros));
+    return n;
 #else
     (void)host;
     (void)max_entries;

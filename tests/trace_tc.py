@@ -26,8 +26,9 @@ def main():
     rows = synth.make_query_rows(n, seed=3)
     ctrl.sdf_eval(rows)                      # warm-up (module load)
     lib = ctrl.lib
-    buf = np.zeros(1 << 16, np.uint64)
-    lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), 1 << 16)   # reset
+    cap = 4 * 3 * 2048
+    buf = np.zeros(cap, np.uint64)
+    lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), cap)   # reset
     import torch
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -36,24 +37,25 @@ def main():
     ctrl.sdf_eval(rows)
     t1.record()
     torch.cuda.synchronize()
-    print(f"{name}: {n} rows, {t0.elapsed_time(t1) * 1e3:.1f} us (with tracing overhead)")
-    cnt = lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), 1 << 16)
-    rec = buf[:cnt]
-    code = (rec >> np.uint64(48)).astype(np.int64)
-    clk = (rec & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
+    print(f"{name}: {n} rows, {t0.elapsed_time(t1) * 1e3:.1f} us (with tracing)")
+    lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), cap)
+    rec = buf.reshape(4, 3, 2048)
     for blk in range(2):
-        sel = ((code >> 14) & 3) == blk
-        c, k = code[sel], clk[sel]
-        order = np.argsort(k, kind="stable")
-        c, k = c[order], k[order]
-        if len(k) == 0:
+        ev = []
+        for role in range(3):
+            r = rec[blk, role]
+            r = r[r != 0]
+            code = (r >> np.uint64(48)).astype(np.int64)
+            clk = (r & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
+            ev += [(int(k), role, int(c)) for k, c in zip(clk, code)]
+        if not ev:
             continue
-        base = k[0]
-        print(f"--- block {blk}: {len(k)} events, span {k[-1] - base} cycles")
-        for ci, ki in zip(c, k):
-            role = ["MMA", "EPI0", "EPI7"][(ci >> 12) & 3]
-            ev = EV.get((ci >> 8) & 15, "?")
-            print(f"{ki - base:8d} {role:5s} {ev:16s} l={(ci >> 6) & 3} h={(ci >> 5) & 1} c={(ci >> 4) & 1} t={ci & 15}")
+        ev.sort()
+        base = ev[0][0]
+        print(f"--- block {blk}: {len(ev)} events, span {ev[-1][0] - base} cycles")
+        for k, role, ci in ev:
+            print(f"{k - base:8d} {['MMA', 'EPI0', 'EPI7'][role]:5s} {EV.get((ci >> 8) & 15, '?'):16s} "
+                  f"l={(ci >> 6) & 3} h={(ci >> 5) & 1} c={(ci >> 4) & 1} t={ci & 15}")
 
 
 if __name__ == "__main__":
