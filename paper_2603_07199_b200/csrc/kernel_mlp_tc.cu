@@ -22,7 +22,7 @@
 // the epilogue of N-half 1. TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2) and
 // A1 [3H/2, 2H) bf16 activations (two per 32-bit column), alternating per layer.
 // Warp roles: warp 0 = TMEM allocator + MMA issuer (one thread of the leader CTA); warp 1 = weight
-// loader; warps 4..11 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column quarter).
+// loader; warps 2..9 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column half of a unit).
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -55,8 +55,8 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 #define TC_TRACE_DECL
 #endif
 
-constexpr int kThreads = 384;
-constexpr int kEpiWarp0 = 4;
+constexpr int kThreads = 320;   // warp 0 MMA, warp 1 weight loader, warps 2..9 epilogue
+constexpr int kEpiWarp0 = 2;    // epilogue warp w reads TMEM lanes 32 (w % 4): warps 2..9 cover each quarter twice
 constexpr int kEpiWarps = 8;
 constexpr int kTileRows = 128;
 
@@ -81,9 +81,11 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// arrive on a barrier given by its shared::cluster address (possibly in the peer CTA)
+// Arrive on a barrier given by its shared::cluster address (possibly in the peer CTA). Default
+// (.release.cta) semantics: the only data ordered through these barriers are TMEM accesses, which the
+// tcgen05.fence::before/after_thread_sync pair orders; a .cluster-scope release fence costs ~1k cycles.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -91,19 +93,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 template <bool kCluster>
 __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
     uint32_t ok;
-    if constexpr (kCluster) {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
-            "selp.b32 %0, 1, 0, P1;\n\t}"
-            : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-            "selp.b32 %0, 1, 0, P1;\n\t}"
-            : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
     return ok != 0;
 }
 // Bounded wait: a schedule bug traps (launch error) instead of hanging the GPU.
@@ -215,15 +209,15 @@ struct Cfg {
     static constexpr int ROWS_B = HALF / CG;                 // weight rows (N) of a unit held per CTA
     static constexpr int UNIT_BYTES = ROWS_B * HALF * 2;     // bf16 B block of one unit in one CTA
     static constexpr int W_BYTES = G * 4 * UNIT_BYTES;       // resident weights per CTA
-    static constexpr int TMEM_COLS = 2 * H;                  // D (H) + two A regions (H/2 each)
-    static constexpr int A0 = H;
+    static constexpr int TMEM_COLS = 2 * H;                  // two tile slots x (D half + A)
+    static constexpr int SLOT_COLS = H;                      // per slot: D [0, HALF) fp32, A [HALF, H) bf16x2
     static constexpr int QW = HALF / 2;                      // epilogue columns per warp per unit
     static constexpr int MMA_M = 128 * CG;
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
     static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 slots][H] float4 (W1p, b1'), scaled
-    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 parity][2 ch][128] partial dots
+    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 slots][2 ch][128] partial dots
     static constexpr int OFF_BAR = OFF_PART + 4 * 2 * 2 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 16;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
@@ -231,11 +225,11 @@ struct Cfg {
 };
 
 // Barrier slots (8 B each)
-enum { BAR_AREADY = 0 /*[2 regions][2 chunks]*/, BAR_DFREE = 4 /*[2]*/, BAR_MMA = 6 /*[2]*/, BAR_WLOCAL = 8,
+enum { BAR_AREADY = 0 /*[2 slots]*/, BAR_DFREE = 4 /*[2 slots]*/, BAR_MMA = 6 /*[2 slots]*/, BAR_WLOCAL = 8,
        BAR_WREADY = 9 };
 
 template <int H, int G, int ACT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(200)
     k_mlp_tc(Params p, const float4* __restrict__ rows, long long n_rows, int ctrl_fixed, int states_mode,
              const uint8_t* __restrict__ wimg, const float* __restrict__ hid_b, const float* __restrict__ w_out,
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
@@ -307,75 +301,70 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 0) {
         // ================= MMA issuer (one thread of the leader CTA)
-        // Units per layer in K-chunk-major order (c0h0, c0h1, c1h0, c1h1): both K-chunk-0 units only
-        // need the first half of the previous layer's activations.
+        // Two tiles in flight (TMEM slots 0/1). Per layer and N-half h, one full-K unit per slot, issued
+        // X(h0) Y(h0) X(h1) Y(h1): while the epilogue drains one slot the tensor pipe works on the other.
         if (lane == 0 && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::HALF);
-            uint32_t stage = 0;            // A stage counter (region = stage & 1)
-            uint32_t d_use[2] = {0, 0};    // uses of D half h so far
+            const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
+            uint32_t a_cnt[2] = {0, 0}, u_cnt[2] = {0, 0};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
-            for (long long tile = group; tile < n_tiles; tile += n_groups) {
-                for (int l = 0; l < G; ++l, ++stage) {
-                    const uint32_t region = stage & 1;
-                    const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
-                    for (int c = 0; c < 2; ++c)
-                        for (int h = 0; h < 2; ++h) {
-                            TC_TRACE(0, 0, l, h, c, tile);
-                            if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + region * 2 + c), (stage >> 1) & 1);
-                            if (c == 0) {
-                                if (d_use[h] > 0) mbar_wait<CG == 2>(bar(BAR_DFREE + h), (d_use[h] - 1) & 1);
-                                ++d_use[h];
-                            }
+            for (long long i0 = 0; i0 < n_my; i0 += 2) {
+                const int ns = i0 + 1 < n_my ? 2 : 1;
+                for (int l = 0; l < G; ++l)
+                    for (int h = 0; h < 2; ++h)
+                        for (int sl = 0; sl < ns; ++sl) {
+                            TC_TRACE(0, 0, l, h, sl, i0);
+                            if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
+                            if (u_cnt[sl] > 0) mbar_wait<CG == 2>(bar(BAR_DFREE + sl), (u_cnt[sl] - 1) & 1);
+                            ++u_cnt[sl];
                             tc_fence_after();
-                            TC_TRACE(0, 1, l, h, c, tile);
-                            const uint32_t b_addr = sbase + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES);
+                            TC_TRACE(0, 1, l, h, sl, i0);
+                            const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
+                            const uint32_t a_t = d_t + (uint32_t)C::HALF;
 #pragma unroll
-                            for (int j = 0; j < C::HALF / 16; ++j) {
-                                const int kk = j * 16;
-                                const uint32_t boff = (uint32_t)((kk / 64) * (C::ROWS_B * 128) + (kk % 64) * 2);
-                                const uint64_t bdesc = smem_desc_sw128(b_addr + boff);
-                                const uint32_t a_t = tmem + a_col + (uint32_t)((c * C::HALF + kk) / 2);
-                                const uint32_t d_t = tmem + (uint32_t)(h * C::HALF);
-                                tc_mma_ts<CG>(d_t, a_t, bdesc, idesc, (c > 0 || j > 0) ? 1u : 0u);
+                            for (int j = 0; j < H / 16; ++j) {
+                                const int kk = j * 16, c = kk / C::HALF, kin = kk % C::HALF;
+                                const uint32_t b_addr = sbase + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES) +
+                                                        (uint32_t)((kin / 64) * (C::ROWS_B * 128) + (kin % 64) * 2);
+                                tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, j > 0 ? 1u : 0u);
                             }
-                            if (c == 1) tc_commit<CG>(bar(BAR_MMA + h));
-                            TC_TRACE(0, 2, l, h, c, tile);
+                            tc_commit<CG>(bar(BAR_MMA + sl));
+                            TC_TRACE(0, 2, l, h, sl, i0);
                         }
-                }
             }
         }
     } else if (warp >= kEpiWarp0) {
         // ================= epilogue (8 warps per CTA)
         const int e = warp - kEpiWarp0;
         const int g = warp & 3;            // TMEM lane quarter
-        const int ch = e >> 2;             // column quarter within an N-half
+        const int ch = e >> 2;             // column half of each N-half (QW columns)
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
         const bool tracer = lane == 0 && (e == 0 || e == 7);
         const int trole = 1 + (e == 7);
-        uint32_t stage = 0;
+        const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
         uint32_t mma_cnt[2] = {0, 0};
-        int t_iter = 0;                    // tiles processed by this CTA (parity of smem double buffers)
         long long staged_lo = -1;   // controllers staged_lo, staged_lo + 1 have (W1p, b1') in s_w1[0], s_w1[1]
         auto arrive_sched = [&](int i) {   // epilogue -> MMA issuer (leader CTA)
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(i));
             else mbar_arrive_local(bar(i));
         };
+        auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
-        auto load_row = [&](long long t) {
-            const long long row = tile_row0(t) + row_in_tile;
+        auto load_row = [&](long long i) {
+            if (i >= n_my) return make_float4(0.f, 0.f, 0.f, 0.f);
+            const long long row = tile_row0(tile_of(i)) + row_in_tile;
             return row < n_rows ? __ldg(rows + row) : make_float4(0.f, 0.f, 0.f, 0.f);
         };
-        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A region of `stage`
-        auto layer1 = [&](long long t1, const float4 q) {
-            if (tracer) TC_TRACE(trole, 6, 0, 0, 0, t1);
+        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of slot sl
+        auto layer1 = [&](long long t1, const float4 q, int sl) {
+            if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
             const long long row0 = tile_row0(t1);
             const long long rlast = min(row0 + kTileRows, n_rows) - 1;
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             const long long hi = states_mode ? rlast / rows_per_ctrl : ctrl_fixed;
-            const bool wide = hi - lo > 1;            // > 2 controllers in one tile (tiny K*T only)
-            if (lo != staged_lo) {   // s_w1 holds controllers lo and lo + 1
-                // uniform across the epilogue warps; the previous tile's layer 1 is behind bar 1
+            if (lo != staged_lo) {   // uniform across the epilogue warps
+                named_bar_sync(2, kEpiWarps * 32);   // nobody still reads the old staging
                 for (int i = threadIdx.x - kEpiWarp0 * 32; i < 2 * H; i += kEpiWarps * 32) {
                     const long long bb = lo + i / H;
                     const int j = i % H;
@@ -390,15 +379,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             const int slot = (int)min(bb - lo, 1ll);
             const float4* wrow = s_w1 + slot * H;
-            const float* bfar = (wide && bb - lo > 1) ? b1f + (size_t)bb * H : nullptr;
-            const uint32_t region = stage & 1;
-            const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
+            const float* bfar = (hi - lo > 1 && bb - lo > 1) ? b1f + (size_t)bb * H : nullptr;
+            const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
+            const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
+#pragma unroll
             for (int c = 0; c < 2; ++c) {
 #pragma unroll
                 for (int q32 = 0; q32 < C::QW / 32; ++q32) {
                     const int j0 = c * C::HALF + ch * C::QW + q32 * 32;
                     uint32_t packed[16];
-                    if (!__any_sync(0xFFFFFFFFu, bfar != nullptr)) {
+                    if (!any_far) {
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
                             const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
@@ -406,8 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
                             packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
                         }
-                    } else {   // rare: rows of a third controller in this tile
-#pragma unroll 1
+                    } else {   // rare (K*T < one tile): rows of a third controller in this tile
+#pragma unroll
                         for (int i = 0; i < 32; i += 2) {
                             const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
                             const float b0 = bfar ? __ldg(bfar + j0 + i) * kP : w0.w;
@@ -419,111 +409,128 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                 }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + c);
             }
-            ++stage;
-            if (tracer) TC_TRACE(trole, 7, 0, 0, 0, t1);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_sched(BAR_AREADY + sl);
+            if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
-        long long tile = group;
-        float4 q_cur = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (tile < n_tiles) {
-            q_cur = load_row(tile);
-            layer1(tile, q_cur);
+        float4 qs[2];
+        for (int sl = 0; sl < 2; ++sl) {
+            qs[sl] = load_row(sl);
+            if (sl < n_my) layer1(tile_of(sl), qs[sl], sl);
         }
-        for (; tile < n_tiles; tile += n_groups, ++t_iter) {
-            const long long next = tile + n_groups;
-            const float4 q_next = next < n_tiles ? load_row(next) : make_float4(0.f, 0.f, 0.f, 0.f);  // prefetch
-            float sdot = 0.f;
+        for (long long i0 = 0; i0 < n_my; i0 += 2) {
+            const int ns = i0 + 1 < n_my ? 2 : 1;
+            const float4 qn[2] = {load_row(i0 + 2), load_row(i0 + 3)};   // prefetch the next pair's rows
+            uint32_t keep[2][C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
+            float sdot[2] = {0.f, 0.f};
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
-                if (last && next < n_tiles) layer1(next, q_next);   // overlaps the last layer's MMAs
-                const uint32_t region = stage & 1;                   // region this layer's output goes to
-                const uint32_t a_col = (uint32_t)C::A0 + region * (H / 2);
                 const float* hb = s_hb + l * H;
+#pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if (tracer) TC_TRACE(trole, 3, l, h, 0, tile);
-                    mbar_wait(bar(BAR_MMA + h), mma_cnt[h] & 1);
-                    ++mma_cnt[h];
-                    tc_fence_after();
-                    if (tracer) TC_TRACE(trole, 4, l, h, 0, tile);
-                    // read all of this warp's accumulator columns of N-half h, then release D[h] at once
-                    uint32_t acc[C::QW / 32][32];
 #pragma unroll
-                    for (int q32 = 0; q32 < C::QW / 32; ++q32)
-                        tmem_ld32(tmem + lane_addr + (uint32_t)(h * C::HALF + ch * C::QW + q32 * 32), acc[q32]);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) arrive_sched(BAR_DFREE + h);
+                    for (int sl = 0; sl < 2; ++sl) {
+                        if (sl >= ns) continue;
+                        if (tracer) TC_TRACE(trole, 3, l, h, sl, i0);
+                        mbar_wait(bar(BAR_MMA + sl), (mma_cnt[sl]++) & 1);
+                        tc_fence_after();
+                        if (tracer) TC_TRACE(trole, 4, l, h, sl, i0);
+                        const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + ch * C::QW);
+                        uint32_t acc[C::QW / 32][32];
 #pragma unroll
-                    for (int q32 = 0; q32 < C::QW / 32; ++q32) {
-                        const int j0 = h * C::HALF + ch * C::QW + q32 * 32;
-                        if (!last) {
-                            uint32_t packed[16];
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4) {
-                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
-                                const float x0 = fmaf(__uint_as_float(acc[q32][i]), kP, bv.x);
-                                const float x1 = fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y);
-                                const float x2 = fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z);
-                                const float x3 = fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w);
-                                packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
-                                packed[i / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
-                            }
-                            tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4) {
-                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
-                                const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
-                                const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i]), kP, bv.x)),
-                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y)));
-                                const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z)),
-                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w)));
-                                sdot = fmaf(__uint_as_float(p0 << 16), wv.x, sdot);
-                                sdot = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot);
-                                sdot = fmaf(__uint_as_float(p1 << 16), wv.z, sdot);
-                                sdot = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot);
-                            }
-                        }
-                    }
-                    if (!last) {
-                        tmem_wait_st();
+                        for (int q32 = 0; q32 < C::QW / 32; ++q32)
+                            tmem_ld32(tmem + lane_addr + d_col + (uint32_t)(q32 * 32), acc[q32]);
+                        tmem_wait_ld();
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) arrive_sched(BAR_AREADY + region * 2 + h);
+                        if (lane == 0) arrive_sched(BAR_DFREE + sl);   // D of this slot may be overwritten now
+                        if (tracer) TC_TRACE(trole, 10, l, h, sl, i0);
+#pragma unroll
+                        for (int q32 = 0; q32 < C::QW / 32; ++q32) {
+                            const int j0 = h * C::HALF + ch * C::QW + q32 * 32;   // output neuron index
+                            if (!last) {
+                                uint32_t* pk = h == 0 ? &keep[sl][q32 * 16] : nullptr;
+                                uint32_t packed[16];
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4) {
+                                    const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
+                                    const float x0 = fmaf(__uint_as_float(acc[q32][i]), kP, bv.x);
+                                    const float x1 = fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y);
+                                    const float x2 = fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z);
+                                    const float x3 = fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w);
+                                    packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                                    packed[i / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
+                                }
+                                if (h == 0) {
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) pk[i] = packed[i];
+                                } else {
+                                    // both N-halves of this layer done: A of the slot is dead -> next input
+                                    const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
+                                    uint32_t k0[16];
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) k0[i] = keep[sl][q32 * 16 + i];
+                                    tmem_st16(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2), k0);
+                                    tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                                }
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4) {
+                                    const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
+                                    const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
+                                    const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i]), kP, bv.x)),
+                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y)));
+                                    const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z)),
+                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w)));
+                                    sdot[sl] = fmaf(__uint_as_float(p0 << 16), wv.x, sdot[sl]);
+                                    sdot[sl] = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot[sl]);
+                                    sdot[sl] = fmaf(__uint_as_float(p1 << 16), wv.z, sdot[sl]);
+                                    sdot[sl] = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot[sl]);
+                                }
+                            }
+                        }
+                        if (!last && h == 1) {
+                            tmem_wait_st();
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) arrive_sched(BAR_AREADY + sl);
+                        }
+                        if (tracer) TC_TRACE(trole, 5, l, h, sl, i0);
+                        if (last && h == 1) {
+                            // ---- output of this slot's tile: combine column halves, FD pair, write
+                            const long long tile = tile_of(i0 + sl);
+                            float* part = s_part + sl * 2 * kTileRows;
+                            part[ch * kTileRows + row_in_tile] = sdot[sl];
+                            named_bar_sync(1, kEpiWarps * 32);
+                            if (ch == 0) {
+                                const float sv = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
+                                const long long row = tile_row0(tile) + row_in_tile;
+                                if (row < n_rows && sdf_out) sdf_out[row] = sv;
+                                if (states_mode) {
+                                    if (p.rps == 2) {
+                                        const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
+                                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
+                                                           p.w_guide * qs[sl].w * (s1 - sv) * p.inv_fd_h;
+                                        if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
+                                    } else {
+                                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
+                                        if (row < n_rows) terms[row] = term;
+                                    }
+                                }
+                            }
+                            if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i0);
+                            // next tile of this slot: its layer 1 overlaps the other slot's last MMAs
+                            qs[sl] = qn[sl];
+                            if (i0 + 2 + sl < n_my) layer1(tile_of(i0 + 2 + sl), qs[sl], sl);
+                        }
                     }
-                    if (tracer) TC_TRACE(trole, 5, l, h, 0, tile);
-                }
-                if (!last) ++stage;
-            }
-            // ---- output: combine the two column quarters, FD pair, write
-            float* part = s_part + (t_iter & 1) * 2 * kTileRows;
-            part[ch * kTileRows + row_in_tile] = sdot;
-            named_bar_sync(1, kEpiWarps * 32);
-            if (ch == 0) {
-                const float s = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
-                const long long row = tile_row0(tile) + row_in_tile;
-                if (row < n_rows && sdf_out) sdf_out[row] = s;
-                if (states_mode) {
-                    if (p.rps == 2) {
-                        const float s1 = __shfl_xor_sync(0xFFFFFFFFu, s, 1);
-                        const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                           p.w_guide * q_cur.w * (s1 - s) * p.inv_fd_h;
-                        if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
-                    } else {
-                        const float term = p.w_sdf * __expf(fminf(-s * p.inv_sdf_scale, p.sdf_exp_max));
-                        if (row < n_rows) terms[row] = term;
-                    }
                 }
             }
-            if (tracer) TC_TRACE(trole, 8, 0, 0, 0, tile);
-            q_cur = q_next;
         }
     }
     // ---- teardown
