@@ -22,7 +22,7 @@
 // the epilogue of N-half 1. TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2) and
 // A1 [3H/2, 2H) bf16 activations (two per 32-bit column), alternating per layer.
 // Warp roles: warp 0 = TMEM allocator + MMA issuer (one thread of the leader CTA); warp 1 = weight
-// loader; warps 2..9 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column half of a unit).
+// loader; warps 4..11 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column half of a unit).
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -55,8 +55,8 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 #define TC_TRACE_DECL
 #endif
 
-constexpr int kThreads = 320;   // warp 0 MMA, warp 1 weight loader, warps 2..9 epilogue
-constexpr int kEpiWarp0 = 2;    // epilogue warp w reads TMEM lanes 32 (w % 4): warps 2..9 cover each quarter twice
+constexpr int kThreads = 384;   // warpgroup 0: MMA, weight loader, 2 idle; warpgroups 1-2: epilogue
+constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
 constexpr int kEpiWarps = 8;
 constexpr int kTileRows = 128;
 
@@ -229,7 +229,7 @@ enum { BAR_AREADY = 0 /*[2 slots]*/, BAR_DFREE = 4 /*[2 slots]*/, BAR_MMA = 6 /*
        BAR_WREADY = 9 };
 
 template <int H, int G, int ACT>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
     k_mlp_tc(Params p, const float4* __restrict__ rows, long long n_rows, int ctrl_fixed, int states_mode,
              const uint8_t* __restrict__ wimg, const float* __restrict__ hid_b, const float* __restrict__ w_out,
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
@@ -441,34 +441,35 @@ __global__ void __maxnreg__(200)
                         tc_fence_after();
                         if (tracer) TC_TRACE(trole, 4, l, h, sl, i0);
                         const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + ch * C::QW);
-                        uint32_t acc[C::QW / 32][32];
-#pragma unroll
-                        for (int q32 = 0; q32 < C::QW / 32; ++q32)
-                            tmem_ld32(tmem + lane_addr + d_col + (uint32_t)(q32 * 32), acc[q32]);
-                        tmem_wait_ld();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) arrive_sched(BAR_DFREE + sl);   // D of this slot may be overwritten now
-                        if (tracer) TC_TRACE(trole, 10, l, h, sl, i0);
+                        // one 32-column TMEM chunk at a time (register budget); D of the slot is released
+                        // after the last chunk's load: the other slot's MMA unit (~1k cycles) covers it.
 #pragma unroll
                         for (int q32 = 0; q32 < C::QW / 32; ++q32) {
+                            uint32_t acc[32];
+                            tmem_ld32(tmem + lane_addr + d_col + (uint32_t)(q32 * 32), acc);
+                            tmem_wait_ld();
+                            if (q32 == C::QW / 32 - 1) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) arrive_sched(BAR_DFREE + sl);
+                                if (tracer) TC_TRACE(trole, 10, l, h, sl, i0);
+                            }
                             const int j0 = h * C::HALF + ch * C::QW + q32 * 32;   // output neuron index
                             if (!last) {
-                                uint32_t* pk = h == 0 ? &keep[sl][q32 * 16] : nullptr;
                                 uint32_t packed[16];
 #pragma unroll
                                 for (int i = 0; i < 32; i += 4) {
                                     const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
-                                    const float x0 = fmaf(__uint_as_float(acc[q32][i]), kP, bv.x);
-                                    const float x1 = fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y);
-                                    const float x2 = fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z);
-                                    const float x3 = fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w);
+                                    const float x0 = fmaf(__uint_as_float(acc[i]), kP, bv.x);
+                                    const float x1 = fmaf(__uint_as_float(acc[i + 1]), kP, bv.y);
+                                    const float x2 = fmaf(__uint_as_float(acc[i + 2]), kP, bv.z);
+                                    const float x3 = fmaf(__uint_as_float(acc[i + 3]), kP, bv.w);
                                     packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
                                     packed[i / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
                                 }
                                 if (h == 0) {
 #pragma unroll
-                                    for (int i = 0; i < 16; ++i) pk[i] = packed[i];
+                                    for (int i = 0; i < 16; ++i) keep[sl][q32 * 16 + i] = packed[i];
                                 } else {
                                     // both N-halves of this layer done: A of the slot is dead -> next input
                                     const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
@@ -483,10 +484,10 @@ __global__ void __maxnreg__(200)
                                 for (int i = 0; i < 32; i += 4) {
                                     const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
                                     const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
-                                    const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i]), kP, bv.x)),
-                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 1]), kP, bv.y)));
-                                    const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 2]), kP, bv.z)),
-                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[q32][i + 3]), kP, bv.w)));
+                                    const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i]), kP, bv.x)),
+                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[i + 1]), kP, bv.y)));
+                                    const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i + 2]), kP, bv.z)),
+                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[i + 3]), kP, bv.w)));
                                     sdot[sl] = fmaf(__uint_as_float(p0 << 16), wv.x, sdot[sl]);
                                     sdot[sl] = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot[sl]);
                                     sdot[sl] = fmaf(__uint_as_float(p1 << 16), wv.z, sdot[sl]);
