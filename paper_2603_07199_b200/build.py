@@ -29,10 +29,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False, extra: tuple = (), suffix: str = "") -> str:
     """trace=True builds the debug variant libmppi_b200_trace.so (-DMPPI_TC_TRACE kernel timeline)."""
-    lib_out = LIB.replace(".so", "_trace.so") if trace else LIB
-    if not force and not trace and not needs_build():
+    lib_out = LIB.replace(".so", ("_trace" if trace else "") + suffix + ".so")
+    if not force and not trace and not suffix and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     cmd = [nvcc, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", inc, "-I", os.path.join(ROOT, "include"),
-           *(["-DMPPI_TC_TRACE"] if trace else []), *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp]
+           *(["-DMPPI_TC_TRACE"] if trace else []), *extra, *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -52,4 +52,6 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    ex = tuple(a for a in sys.argv[1:] if a.startswith("-D"))
+    sfx = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--suffix=")), "")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv, extra=ex, suffix=sfx))

@@ -22,7 +22,7 @@
 // the epilogue of N-half 1. TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2) and
 // A1 [3H/2, 2H) bf16 activations (two per 32-bit column), alternating per layer.
 // Warp roles: warp 0 = TMEM allocator + MMA issuer (one thread of the leader CTA); warp 1 = weight
-// loader; warps 4..11 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column half of a unit).
+// loader; warps 4..19 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column quarter of a unit).
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -55,9 +55,14 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 #define TC_TRACE_DECL
 #endif
 
-constexpr int kThreads = 384;   // warpgroup 0: MMA, weight loader, 2 idle; warpgroups 1-2: epilogue
+#ifndef MPPI_EPI_WARPS
+#define MPPI_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = MPPI_EPI_WARPS;   // 8 or 16 (2 or 4 per SMSP)
 constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
-constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 weight loader, 2-3 idle
+constexpr int kColGroups = kEpiWarps / 4;   // column groups per TMEM lane quarter
+constexpr int kCW = 16;         // TMEM columns per epilogue load (register budget: 96/thread)
 constexpr int kTileRows = 128;
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -154,6 +159,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
@@ -211,14 +229,16 @@ struct Cfg {
     static constexpr int W_BYTES = G * 4 * UNIT_BYTES;       // resident weights per CTA
     static constexpr int TMEM_COLS = 2 * H;                  // two tile slots x (D half + A)
     static constexpr int SLOT_COLS = H;                      // per slot: D [0, HALF) fp32, A [HALF, H) bf16x2
-    static constexpr int QW = HALF / 2;                      // epilogue columns per warp per unit
+    static constexpr int QW = HALF / kColGroups;             // epilogue columns per warp per unit
+    static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
     static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 slots][H] float4 (W1p, b1'), scaled
-    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 slots][2 ch][128] partial dots
-    static constexpr int OFF_BAR = OFF_PART + 4 * 2 * 2 * kTileRows;
+    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 slots][col groups][128] partial dots
+    static constexpr int OFF_ROWS = OFF_PART + 4 * 2 * kColGroups * kTileRows;  // [4 bufs][128] float4 query rows
+    static constexpr int OFF_BAR = OFF_ROWS + 4 * 16 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 16;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
     static_assert(SMEM <= 232448, "shared memory budget");
@@ -226,7 +246,7 @@ struct Cfg {
 
 // Barrier slots (8 B each)
 enum { BAR_AREADY = 0 /*[2 slots]*/, BAR_DFREE = 4 /*[2 slots]*/, BAR_MMA = 6 /*[2 slots]*/, BAR_WLOCAL = 8,
-       BAR_WREADY = 9 };
+       BAR_WREADY = 9, BAR_ROWS = 10 /*[4 row buffers]*/ };
 
 template <int H, int G, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -265,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kEpiWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
+        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_ROWS + i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -334,14 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ================= epilogue (8 warps per CTA)
+        // ================= epilogue (16 warps per CTA)
         const int e = warp - kEpiWarp0;
         const int g = warp & 3;            // TMEM lane quarter
-        const int ch = e >> 2;             // column half of each N-half (QW columns)
+        const int cgi = e >> 2;            // column group of each N-half (QW columns)
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
-        const bool tracer = lane == 0 && (e == 0 || e == 7);
-        const int trole = 1 + (e == 7);
+        const bool tracer = lane == 0 && (e == 0 || e == kEpiWarps - 1);
+        const int trole = 1 + (e == kEpiWarps - 1);
         const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
         uint32_t mma_cnt[2] = {0, 0};
         long long staged_lo = -1;   // controllers staged_lo, staged_lo + 1 have (W1p, b1') in s_w1[0], s_w1[1]
@@ -351,14 +372,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
-        auto load_row = [&](long long i) {
-            if (i >= n_my) return make_float4(0.f, 0.f, 0.f, 0.f);
-            const long long row = tile_row0(tile_of(i)) + row_in_tile;
-            return row < n_rows ? __ldg(rows + row) : make_float4(0.f, 0.f, 0.f, 0.f);
+        // query rows of this CTA's part of tile i -> smem buffer i & 3 by one bulk-async copy (TMA engine),
+        // issued two tiles ahead by one elected epilogue thread
+        const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS);
+        const bool row_issuer = e == 0 && lane == 0;
+        auto issue_rows = [&](long long i) {
+            if (!row_issuer || i >= n_my) return;
+            const long long r0 = tile_row0(tile_of(i));
+            const long long nv = min((long long)kTileRows, n_rows - r0);
+            if (nv <= 0) {
+                mbar_arrive_local(bar(BAR_ROWS + (int)(i & 3)));
+                return;
+            }
+            mbar_expect_tx(bar(BAR_ROWS + (int)(i & 3)), (uint32_t)(16 * nv));
+            bulk_g2s(sbase + C::OFF_ROWS + (uint32_t)((i & 3) * 16 * kTileRows), rows + r0, (uint32_t)(16 * nv),
+                     bar(BAR_ROWS + (int)(i & 3)));
         };
-        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of slot sl
-        auto layer1 = [&](long long t1, const float4 q, int sl) {
+        auto row_of = [&](long long i) {   // this thread's query row of tile i (after its buffer landed)
+            const long long row = tile_row0(tile_of(i)) + row_in_tile;
+            return row < n_rows ? s_rows[(i & 3) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of slot sl, for tile index i
+        auto layer1 = [&](long long i, int sl) {
+            const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
+            mbar_wait(bar(BAR_ROWS + (int)(i & 3)), (uint32_t)((i >> 2) & 1));
+            const float4 q = row_of(i);
+            issue_rows(i + 2);   // buffer (i+2)&3 was last read by tile i-2's layer 1 (behind bar 1)
             const long long row0 = tile_row0(t1);
             const long long rlast = min(row0 + kTileRows, n_rows) - 1;
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
@@ -385,12 +425,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
 #pragma unroll
-                for (int q32 = 0; q32 < C::QW / 32; ++q32) {
-                    const int j0 = c * C::HALF + ch * C::QW + q32 * 32;
-                    uint32_t packed[16];
+                for (int k = 0; k < C::NCH; ++k) {
+                    const int j0 = c * C::HALF + cgi * C::QW + k * kCW;
+                    uint32_t packed[kCW / 2];
                     if (!any_far) {
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
+                        for (int i = 0; i < kCW; i += 2) {
                             const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
                             const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, w0.w)));
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
@@ -398,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     } else {   // rare (K*T < one tile): rows of a third controller in this tile
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
+                        for (int i = 0; i < kCW; i += 2) {
                             const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
                             const float b0 = bfar ? __ldg(bfar + j0 + i) * kP : w0.w;
                             const float b1 = bfar ? __ldg(bfar + j0 + i + 1) * kP : w1.w;
@@ -407,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
                         }
                     }
-                    tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                 }
             }
             tmem_wait_st();
@@ -417,14 +457,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
-        float4 qs[2];
-        for (int sl = 0; sl < 2; ++sl) {
-            qs[sl] = load_row(sl);
-            if (sl < n_my) layer1(tile_of(sl), qs[sl], sl);
-        }
+        issue_rows(0);
+        issue_rows(1);
+        for (int sl = 0; sl < 2; ++sl)
+            if (sl < n_my) layer1(sl, sl);
         for (long long i0 = 0; i0 < n_my; i0 += 2) {
             const int ns = i0 + 1 < n_my ? 2 : 1;
-            const float4 qn[2] = {load_row(i0 + 2), load_row(i0 + 3)};   // prefetch the next pair's rows
             uint32_t keep[2][C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
             float sdot[2] = {0.f, 0.f};
 #pragma unroll 1
@@ -440,25 +478,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(bar(BAR_MMA + sl), (mma_cnt[sl]++) & 1);
                         tc_fence_after();
                         if (tracer) TC_TRACE(trole, 4, l, h, sl, i0);
-                        const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + ch * C::QW);
-                        // one 32-column TMEM chunk at a time (register budget); D of the slot is released
+                        const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
+                        const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
+                        // one 16-column TMEM chunk at a time (register budget); D of the slot is released
                         // after the last chunk's load: the other slot's MMA unit (~1k cycles) covers it.
 #pragma unroll
-                        for (int q32 = 0; q32 < C::QW / 32; ++q32) {
-                            uint32_t acc[32];
-                            tmem_ld32(tmem + lane_addr + d_col + (uint32_t)(q32 * 32), acc);
+                        for (int k = 0; k < C::NCH; ++k) {
+                            uint32_t acc[kCW];
+                            tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
                             tmem_wait_ld();
-                            if (q32 == C::QW / 32 - 1) {
+                            if (k == C::NCH - 1) {
                                 tc_fence_before();
                                 __syncwarp();
                                 if (lane == 0) arrive_sched(BAR_DFREE + sl);
                                 if (tracer) TC_TRACE(trole, 10, l, h, sl, i0);
                             }
-                            const int j0 = h * C::HALF + ch * C::QW + q32 * 32;   // output neuron index
+                            const int j0 = h * C::HALF + cgi * C::QW + k * kCW;   // output neuron index
                             if (!last) {
-                                uint32_t packed[16];
+                                uint32_t packed[kCW / 2];
 #pragma unroll
-                                for (int i = 0; i < 32; i += 4) {
+                                for (int i = 0; i < kCW; i += 4) {
                                     const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
                                     const float x0 = fmaf(__uint_as_float(acc[i]), kP, bv.x);
                                     const float x1 = fmaf(__uint_as_float(acc[i + 1]), kP, bv.y);
@@ -469,19 +508,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                                 if (h == 0) {
 #pragma unroll
-                                    for (int i = 0; i < 16; ++i) keep[sl][q32 * 16 + i] = packed[i];
+                                    for (int i = 0; i < kCW / 2; ++i) keep[sl][k * (kCW / 2) + i] = packed[i];
                                 } else {
                                     // both N-halves of this layer done: A of the slot is dead -> next input
-                                    const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
-                                    uint32_t k0[16];
-#pragma unroll
-                                    for (int i = 0; i < 16; ++i) k0[i] = keep[sl][q32 * 16 + i];
-                                    tmem_st16(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2), k0);
-                                    tmem_st16(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2),
+                                             &keep[sl][k * (kCW / 2)]);
+                                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                                 }
                             } else {
 #pragma unroll
-                                for (int i = 0; i < 32; i += 4) {
+                                for (int i = 0; i < kCW; i += 4) {
                                     const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
                                     const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
                                     const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i]), kP, bv.x)),
@@ -503,20 +539,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (tracer) TC_TRACE(trole, 5, l, h, sl, i0);
                         if (last && h == 1) {
-                            // ---- output of this slot's tile: combine column halves, FD pair, write
+                            // ---- output of this slot's tile: combine column groups, FD pair, write
                             const long long tile = tile_of(i0 + sl);
-                            float* part = s_part + sl * 2 * kTileRows;
-                            part[ch * kTileRows + row_in_tile] = sdot[sl];
+                            float* part = s_part + sl * kColGroups * kTileRows;
+                            part[cgi * kTileRows + row_in_tile] = sdot[sl];
                             named_bar_sync(1, kEpiWarps * 32);
-                            if (ch == 0) {
-                                const float sv = part[row_in_tile] + part[kTileRows + row_in_tile] + __ldg(b_out);
+                            if (cgi == 0) {
+                                float sv = __ldg(b_out);
+#pragma unroll
+                                for (int q = 0; q < kColGroups; ++q) sv += part[q * kTileRows + row_in_tile];
                                 const long long row = tile_row0(tile) + row_in_tile;
                                 if (row < n_rows && sdf_out) sdf_out[row] = sv;
                                 if (states_mode) {
                                     if (p.rps == 2) {
                                         const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
                                         const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                                           p.w_guide * qs[sl].w * (s1 - sv) * p.inv_fd_h;
+                                                           p.w_guide * row_of(i0 + sl).w * (s1 - sv) * p.inv_fd_h;
                                         if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
                                     } else {
                                         const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
@@ -526,8 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i0);
                             // next tile of this slot: its layer 1 overlaps the other slot's last MMAs
-                            qs[sl] = qn[sl];
-                            if (i0 + 2 + sl < n_my) layer1(tile_of(i0 + 2 + sl), qs[sl], sl);
+                            if (i0 + 2 + sl < n_my) layer1(i0 + 2 + sl, sl);
                         }
                     }
                 }
