@@ -272,7 +272,7 @@ def main():
         e2e_s = float(t.item())
     e2e_value = units_per_step * args.steps / e2e_s
 
-    kt = np.median(np.array(ktimes), 0)            # per-stage ms (noise, rollout, mlp, cost, update)
+    kt = np.median(np.array(ktimes), 0)            # per-stage ms (noise, rollout, mlp, softmin, exchange)
     peaks, peak_src = measured_peaks()
     rows = lcfg.n_ctrl * lcfg.K * lcfg.T * (2 if cfg.fd else 1)
     flop = mlp_flops_per_row(cfg) * rows
@@ -285,7 +285,7 @@ def main():
                 "peak_source": f"{peak_src} bf16 dense (burst)", "traffic": traffic,
                 "algorithmic_flop_per_launch": flop, "flop_per_row": mlp_flops_per_row(cfg), "rows_per_launch": rows,
                 "mlp_share_of_step": mlp_ms / float(np.sum(kt)),
-                "stage_ms": {k: float(v) for k, v in zip(["noise_shift", "rollout", "sdf_mlp", "cost_min", "update"], kt)}}
+                "stage_ms": {k: float(v) for k, v in zip(["noise_shift", "rollout", "sdf_mlp", "softmin_update", "exchange"], kt)}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if sharded or cfg.name == "c4" else "weak", "vs_baseline": None, "dtype": "bf16",

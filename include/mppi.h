@@ -117,8 +117,9 @@ mppi_status mppi_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_
 mppi_status mppi_step_device(mppi_ctx* ctx, const float* d_x0, const float* d_goal, uint64_t step_index);
 
 /* Split-phase sharded step (configs[3] without an NCCL communicator, e.g. emulated ranks):
- * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, V_r[T][4]) per controller;
- * mppi_record_size() is the record length in floats per controller (2 + 4T); mppi_get_record_device()
+ * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, S2_r, V_r[T][4]) per
+ * controller (S2 = sum of squared weights, for the ESS diagnostic); mppi_record_size() is the record
+ * length in floats per controller (3 + 4T); mppi_get_record_device()
  * returns the device pointer of [n_ctrl][record]; mppi_step_finish combines R gathered records
  * (device [R][n_ctrl][record], rank order) into U*. */
 mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step_index);
@@ -138,9 +139,9 @@ mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out);
  * MPPI_DBG_QUERIES: [n_ctrl][T][K][rps][4] query rows (p_c, |v|) / (p_c + h d, 0), rps = 2 if w_guide != 0
  * MPPI_DBG_SDF:     [n_ctrl][T][K][rps] s per row     MPPI_DBG_COSTS: [n_ctrl][K] J
  * MPPI_DBG_NOISE:   [T][n_ctrl*K][4] standard normals used   MPPI_DBG_TERMS: [n_ctrl][T][K] SDF stage terms
- * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums */
+ * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums   MPPI_DBG_RECORD: [n_ctrl][3 + 4T] this rank's record */
 enum { MPPI_DBG_QUERIES = 0, MPPI_DBG_SDF = 1, MPPI_DBG_COSTS = 2, MPPI_DBG_NOISE = 3, MPPI_DBG_TERMS = 4,
-       MPPI_DBG_PARTIAL = 5 };
+       MPPI_DBG_PARTIAL = 5, MPPI_DBG_RECORD = 6 };
 mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes);
 
 /* Test support: run the production SDF-MLP kernel of this context on n query-frame rows
@@ -150,7 +151,8 @@ mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int6
 
 /* Profiling: when on, every step records CUDA events between its kernels (on cfg.stream);
  * mppi_get_kernel_times() synchronises and returns the last step's per-stage device times in ms:
- * out[0] noise+shift, [1] rollout, [2] SDF-MLP, [3] cost+min, [4] update (+exchange). n_out <= 5. */
+ * out[0] noise+shift, [1] rollout, [2] SDF-MLP, [3] softmin (cost + min + weights + update or record),
+ * [4] NCCL exchange + combine (0 unless sharded with NCCL). n_out <= 5. */
 mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t on);
 mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out);
 /* Number of kernels this library launches per mppi_step (for the bench's gpu_launches count). */

@@ -15,7 +15,7 @@ MPPI_ABI_VERSION = 1
 STATUS = {0: "OK", -1: "INVALID", -2: "CUDA", -3: "NCCL", -4: "NOT_READY", -5: "NONFINITE", -6: "OOM",
           -7: "POISONED", -8: "UNSUPPORTED"}
 MPPI_OK, MPPI_ERR_INVALID, MPPI_ERR_NONFINITE, MPPI_ERR_UNSUPPORTED = 0, -1, -5, -8
-DBG = {"queries": 0, "sdf": 1, "costs": 2, "noise": 3, "terms": 4, "partial": 5}
+DBG = {"queries": 0, "sdf": 1, "costs": 2, "noise": 3, "terms": 4, "partial": 5, "record": 6}
 
 # every symbol include/mppi.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["mppi_workspace_bytes", "mppi_create", "mppi_destroy", "mppi_get_nccl_unique_id",

@@ -7,7 +7,7 @@
 //   K1  U^m = U* + dU^m, clamp; rollout xdot = f(x,u)        PAPER.md:139, :146 (CTBR per BASELINE configs[0])
 //       query in the cached frame p_c = R p + t
 //   K2f s = g_phi(z, p_c) with the latent folded into b1'
-//   K3  J = sum of stage costs (Eq. 10 structure)
+//   K3  J = sum of stage costs (Eq. 10 structure)            PAPER.md:185    } fused: k_softmin
 //   K4  U* = sum_m w_m U^m, w = softmax(-J/lambda)           PAPER.md:141 (Eq. 5)
 #include <math.h>
 #include <stdint.h>
@@ -27,14 +27,6 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
         const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
         c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
     }
-}
-
-__device__ __forceinline__ unsigned enc_ordered(float f) {
-    const unsigned u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float dec_ordered(unsigned e) {
-    return __uint_as_float((e & 0x80000000u) ? (e & 0x7FFFFFFFu) : ~e);
 }
 
 __device__ __forceinline__ float act_f32(int a, float x) {
@@ -68,11 +60,13 @@ __global__ void __launch_bounds__(256) k_noise_shift(Params p, Buffers b, int ge
         const float s23 = 1.1920928955078125e-07f;  // 2^-23
         const float u0 = ((float)(c[0] >> 9) + 0.5f) * s23, u1 = ((float)(c[1] >> 9) + 0.5f) * s23;
         const float u2 = ((float)(c[2] >> 9) + 0.5f) * s23, u3 = ((float)(c[3] >> 9) + 0.5f) * s23;
-        const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+        // fast SFU forms (MUFU.LG2 / SIN / COS, abs error ~2^-21 on these ranges):
+        // cos(2 pi u) = -cos(theta), sin(2 pi u) = -sin(theta), theta = 2 pi (u - 1/2) in [-pi, pi)
+        const float r0 = sqrtf(-2.f * __logf(u0)), r1 = sqrtf(-2.f * __logf(u2));
         float s0, c0, s1, c1;
-        sincospif(2.f * u1, &s0, &c0);
-        sincospif(2.f * u3, &s1, &c1);
-        b.noise[i] = make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+        __sincosf(6.283185307179586f * (u1 - 0.5f), &s0, &c0);
+        __sincosf(6.283185307179586f * (u3 - 0.5f), &s1, &c1);
+        b.noise[i] = make_float4(-r0 * c0, -r0 * s0, -r1 * c1, -r1 * s1);
     }
 }
 
@@ -100,7 +94,6 @@ __device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, fl
 __global__ void __launch_bounds__(128) k_rollout(Params p, Buffers b) {
     const int bb = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k == 0) b.jmin_bits[bb] = 0xFFFFFFFFu;   // reset for K3's atomicMin
     if (k >= p.K) return;
     const float* x0 = b.x0 + bb * 10;
     float x[10];
@@ -246,12 +239,40 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
     }
 }
 
-// ------------------------------------------------------------------ K3: cost + min
-// J_k = partial_k + sum_t term[t][k]; non-finite -> +inf; J_min per controller via warp shuffles,
-// then one atomicMin per block on an order-preserving unsigned encoding (deterministic).
-__global__ void __launch_bounds__(256) k_cost_min(Params p, Buffers b) {
-    const int bb = blockIdx.y;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// ------------------------------------------------------------------ K3+K4: cost, softmin weights, update
+// One kernel, grid (sample chunks of 256, controllers). Per block (chunk of samples):
+//   J_k = partial_k + sum_t term[t][k] (non-finite -> +inf)                         PAPER.md:185 (Eq. 10)
+//   m_b = min_k J_k; w_k = exp((m_b - J_k)/lambda); S_b = sum w; S2_b = sum w^2;
+//   V_b[t] = sum_k w_k (clamp(U*_t + sigma n_{t,k}) - U*_t)   (clamped samples, reading R5)
+// -> block record (m_b, S_b, S2_b, V_b). The last block of the controller (atomic ticket) combines the
+// records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
+// U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
+// write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
+constexpr int kSoftminBlock = 256;
+
+__device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float u = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = is_min ? fminf(v, u) : v + u;
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    float r = red[0];
+    for (int i = 1; i < nw; ++i) r = is_min ? fminf(r, red[i]) : r + red[i];   // fixed order
+    return r;
+}
+
+__global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, int write_record) {
+    __shared__ float s_w[kSoftminBlock];
+    __shared__ float red[kSoftminBlock / 32];
+    __shared__ bool s_last;
+    const int bb = blockIdx.y, nblk = gridDim.x;
+    const int k = blockIdx.x * kSoftminBlock + threadIdx.x;
+    const int W = 3 + 4 * p.T;
+    // ---- phase 1: thread per sample
     float J = INFINITY;
     if (k < p.K) {
         float acc = b.partial[(long long)bb * p.K + k];
@@ -260,101 +281,99 @@ __global__ void __launch_bounds__(256) k_cost_min(Params p, Buffers b) {
         J = isfinite(acc) ? acc : INFINITY;
         b.J[(long long)bb * p.K + k] = J;
     }
-    unsigned e = __reduce_min_sync(0xFFFFFFFFu, enc_ordered(J));
-    __shared__ unsigned wmin[8];
-    if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = e;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned m = wmin[0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = min(m, wmin[w]);
-        atomicMin(b.jmin_bits + bb, m);
+    const float m = block_reduce(J, red, true);
+    const float w = (J < INFINITY) ? expf((m - J) * p.inv_lambda) : 0.f;
+    s_w[threadIdx.x] = w;
+    const float S = block_reduce(w, red, false);
+    const float S2 = block_reduce(w * w, red, false);
+    float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
+    if (threadIdx.x == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; }
+    // ---- phase 2: thread per time step, sequential over the block's samples (deterministic)
+    const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
+    const long long NK = (long long)p.n_ctrl * p.K;
+    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+        const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+        const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+        if (m < INFINITY)
+            for (int i = 0; i < kn; ++i) {
+                const float wi = s_w[i];
+                if (wi == 0.f) continue;
+                const float4 n = nz[i];
+                v0 = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v0);
+                v1 = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v1);
+                v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
+                v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
+            }
+        reinterpret_cast<float4*>(rec + 3)[t] = make_float4(v0, v1, v2, v3);
     }
-}
-
-void launch_cost_min(const Params& p, const Buffers& b, cudaStream_t s) {
-    dim3 grid((p.K + 255) / 256, p.n_ctrl);
-    k_cost_min<<<grid, 256, 0, s>>>(p, b);
-}
-
-// ------------------------------------------------------------------ K4: softmin weights + update
-// Block (t, controller): w_k = exp((J_min - J_k)/lambda); S = sum w; V_t = sum w (u_{k,t} - U*_t)
-// with u the clamped sample (reading R5); deterministic tree (shuffles, then fixed-order warps).
-// write_record: store the shard record (m_r, S_r, V_r) instead of updating (configs[3]).
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    return v;
-}
-
-__global__ void __launch_bounds__(256) k_update(Params p, Buffers b, int write_record) {
-    const int t = blockIdx.x, bb = blockIdx.y;
-    const float jmin = dec_ordered(b.jmin_bits[bb]);
-    const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
-    const bool ok = isfinite(jmin);
-    float S = 0.f, S2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-    if (ok) {
-        const float* J = b.J + (long long)bb * p.K;
-        const float4* nz = b.noise + (long long)t * p.n_ctrl * p.K + (long long)bb * p.K;
-        for (int k = threadIdx.x; k < p.K; k += blockDim.x) {
-            const float Jk = J[k];
-            const float w = Jk < INFINITY ? expf((jmin - Jk) * p.inv_lambda) : 0.f;
-            const float4 n = nz[k];
-            S += w;
-            S2 += w * w;
-            v0 += w * (clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x);
-            v1 += w * (clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y);
-            v2 += w * (clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z);
-            v3 += w * (clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w);
+    // ---- last block of this controller combines the block records in order
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(b.tickets + bb, 1u) == (unsigned)(nblk - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float* recs = b.blkrec + (long long)bb * nblk * W;
+    float mg = INFINITY;
+    for (int i = 0; i < nblk; ++i) mg = fminf(mg, __ldcg(recs + (long long)i * W));
+    const bool ok = mg < INFINITY;
+    // S, S2 (thread 0 reads them back; the combine order is fixed)
+    float Sg = 0.f, S2g = 0.f;
+    if (ok)
+        for (int i = 0; i < nblk; ++i) {
+            const float* r = recs + (long long)i * W;
+            const float mi = __ldcg(r);
+            if (!(mi < INFINITY)) continue;
+            const float f = expf((mg - mi) * p.inv_lambda);
+            Sg += __ldcg(r + 1) * f;
+            S2g += __ldcg(r + 2) * f * f;
+        }
+    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+        float4 V = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok)
+            for (int i = 0; i < nblk; ++i) {
+                const float* r = recs + (long long)i * W;
+                const float mi = __ldcg(r);
+                if (!(mi < INFINITY)) continue;
+                const float f = expf((mg - mi) * p.inv_lambda);
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(r + 3) + t);
+                V.x = fmaf(v.x, f, V.x); V.y = fmaf(v.y, f, V.y); V.z = fmaf(v.z, f, V.z); V.w = fmaf(v.w, f, V.w);
+            }
+        if (write_record) {
+            float* out = b.record + (long long)bb * W;
+            reinterpret_cast<float4*>(out + 3)[t] = V;
+        } else {
+            const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+            float4 Un = U;
+            if (ok && Sg > 0.f) {
+                Un.x = U.x + V.x / Sg; Un.y = U.y + V.y / Sg; Un.z = U.z + V.z / Sg; Un.w = U.w + V.w / Sg;
+            }
+            reinterpret_cast<float4*>(b.U_out)[(long long)bb * p.T + t] = Un;
         }
     }
-    __shared__ float red[8][6];
-    float vals[6] = {S, S2, v0, v1, v2, v3};
-#pragma unroll
-    for (int q = 0; q < 6; ++q) vals[q] = warp_sum(vals[q]);
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int q = 0; q < 6; ++q) red[w][q] = vals[q];
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int q = 0; q < 6; ++q) {
-        float a = red[0][q];
-        for (int i = 1; i < nw; ++i) a += red[i][q];
-        vals[q] = a;
-    }
-    S = vals[0];
-    S2 = vals[1];
-    if (write_record) {
-        float* rec = b.record + (long long)bb * (2 + 4 * p.T);
-        if (t == 0) { rec[0] = jmin; rec[1] = S; }
-        rec[2 + 4 * t + 0] = vals[2];
-        rec[2 + 4 * t + 1] = vals[3];
-        rec[2 + 4 * t + 2] = vals[4];
-        rec[2 + 4 * t + 3] = vals[5];
-        return;
-    }
-    float4 Un = U;
-    if (ok && S > 0.f) {
-        Un.x = U.x + vals[2] / S;
-        Un.y = U.y + vals[3] / S;
-        Un.z = U.z + vals[4] / S;
-        Un.w = U.w + vals[5] / S;
-    }
-    reinterpret_cast<float4*>(b.U_out)[(long long)bb * p.T + t] = Un;
-    if (t == 0) {
-        float* d = b.diag + bb * 4;
-        d[0] = jmin;
-        d[1] = S;
-        d[2] = S2 > 0.f ? S * S / S2 : 0.f;
-        d[3] = ok ? 0.f : 1.f;
-        b.flags[bb] = ok ? 0 : 1;
+    if (threadIdx.x == 0) {
+        if (write_record) {
+            float* out = b.record + (long long)bb * W;
+            out[0] = mg; out[1] = Sg; out[2] = S2g;
+        } else {
+            float* d = b.diag + bb * 4;
+            d[0] = mg;
+            d[1] = Sg;
+            d[2] = S2g > 0.f ? Sg * Sg / S2g : 0.f;
+            d[3] = ok ? 0.f : 1.f;
+            b.flags[bb] = ok ? 0 : 1;
+        }
+        b.tickets[bb] = 0u;   // ready for the next step (kernel boundary orders it)
     }
 }
 
-void launch_update(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
-    dim3 grid(p.T, p.n_ctrl);
-    k_update<<<grid, 256, 0, s>>>(p, b, write_record ? 1 : 0);
+void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
+    dim3 grid((p.K + kSoftminBlock - 1) / kSoftminBlock, p.n_ctrl);
+    k_softmin<<<grid, kSoftminBlock, 0, s>>>(p, b, write_record ? 1 : 0);
 }
+
+int softmin_blocks(int K) { return (K + kSoftminBlock - 1) / kSoftminBlock; }
 
 // ------------------------------------------------------------------ shard combine (configs[3])
 // m = min_r m_r; S = sum_r S_r e^{-(m_r - m)/lambda}; V = sum_r V_r e^{...}; U* = U + V/S.
@@ -363,19 +382,20 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n_ctrl * p.T) return;
     const int bb = i / p.T, t = i % p.T;
-    const int W = 2 + 4 * p.T;
+    const int W = 3 + 4 * p.T;
     float m = INFINITY;
     for (int r = 0; r < R; ++r) m = fminf(m, recs[((long long)r * p.n_ctrl + bb) * W]);
     const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
     float4 Un = U;
-    float S = 0.f, v[4] = {0.f, 0.f, 0.f, 0.f};
+    float S = 0.f, S2 = 0.f, v[4] = {0.f, 0.f, 0.f, 0.f};
     if (isfinite(m)) {
         for (int r = 0; r < R; ++r) {
             const float* rec = recs + ((long long)r * p.n_ctrl + bb) * W;
             if (!(rec[0] < INFINITY)) continue;
             const float f = expf((m - rec[0]) * p.inv_lambda);
             S += rec[1] * f;
-            for (int c = 0; c < 4; ++c) v[c] += rec[2 + 4 * t + c] * f;
+            S2 += rec[2] * f * f;
+            for (int c = 0; c < 4; ++c) v[c] += rec[3 + 4 * t + c] * f;
         }
         if (S > 0.f) {
             Un.x = U.x + v[0] / S; Un.y = U.y + v[1] / S; Un.z = U.z + v[2] / S; Un.w = U.w + v[3] / S;
@@ -386,7 +406,7 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
         float* d = b.diag + bb * 4;
         d[0] = m;
         d[1] = S;
-        d[2] = 0.f;   // ESS needs sum w^2 over all shards; not part of the record
+        d[2] = S2 > 0.f ? S * S / S2 : 0.f;
         d[3] = isfinite(m) ? 0.f : 1.f;
         b.flags[bb] = isfinite(m) ? 0 : 1;
     }

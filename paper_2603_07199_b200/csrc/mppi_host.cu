@@ -33,7 +33,7 @@ struct Layout {
 
 enum BufId {
     B_W1P, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
-    B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_JMIN, B_REC, B_GATH, B_DIAG, B_FLAGS, B_COUNT
+    B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_TICK, B_BLKREC, B_REC, B_GATH, B_DIAG, B_FLAGS, B_COUNT
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -43,7 +43,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     const size_t Ld = (size_t)c->latent_dim, G = (size_t)(c->n_hidden - 1);
     const size_t rps = c->w_guide != 0.f ? 2 : 1;
     const size_t world = (size_t)(c->world_size > 0 ? c->world_size : 1);
-    const size_t recw = 2 + 4 * T;
+    const size_t recw = 3 + 4 * T;
     size_t sz[B_COUNT];
     sz[B_W1P] = 16 * H;
     sz[B_W1Z] = 4 * H * Ld;
@@ -67,7 +67,8 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_TERMS] = 4 * n * T * K;
     sz[B_PART] = 4 * n * K;
     sz[B_J] = 4 * n * K;
-    sz[B_JMIN] = 4 * n;
+    sz[B_TICK] = 4 * n;
+    sz[B_BLKREC] = 4 * n * (size_t)softmin_blocks(c->K) * recw;
     sz[B_REC] = 4 * n * recw;
     sz[B_GATH] = 4 * world * n * recw;
     sz[B_DIAG] = 16 * n;
@@ -239,7 +240,8 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     b.terms = (float*)(base + L.off[B_TERMS]);
     b.partial = (float*)(base + L.off[B_PART]);
     b.J = (float*)(base + L.off[B_J]);
-    b.jmin_bits = (unsigned*)(base + L.off[B_JMIN]);
+    b.tickets = (unsigned*)(base + L.off[B_TICK]);
+    b.blkrec = (float*)(base + L.off[B_BLKREC]);
     b.record = (float*)(base + L.off[B_REC]);
     b.gathered = (float*)(base + L.off[B_GATH]);
     b.diag = (float*)(base + L.off[B_DIAG]);
@@ -277,7 +279,11 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess)
         return cleanup(MPPI_ERR_CUDA, "work stream / events");
     // zero-init the small state (U, diag, flags, step) so debug reads are defined
-    if (cudaMemsetAsync(base, 0, L.off[B_NOISE], ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "memset");
+    if (cudaMemsetAsync(base, 0, L.off[B_NOISE], ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(b.tickets, 0, 4 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(b.diag, 0, 16 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(b.flags, 0, 4 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess)
+        return cleanup(MPPI_ERR_CUDA, "memset");
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "sync");
     if (cfg->world_size > 1 && cfg->nccl_unique_id) {
         ncclUniqueId id;
@@ -435,19 +441,19 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     cudaError_t e = launch_mlp_states(ctx, s);
     if (e != cudaSuccess) return e;
     mark(3);
-    launch_cost_min(p, ctx->b, s);
-    mark(4);
     const bool sharded = ctx->cfg.world_size > 1;
     if (mode == 1 || (sharded && ctx->comm)) {
-        launch_update(p, ctx->b, true, s);
+        launch_softmin(p, ctx->b, true, s);
+        mark(4);
         if (mode == 0) {
-            const size_t recn = (size_t)p.n_ctrl * (2 + 4 * p.T);
+            const size_t recn = (size_t)p.n_ctrl * (3 + 4 * p.T);
             if (ncclAllGather(ctx->b.record, ctx->b.gathered, recn, ncclFloat, ctx->comm, s) != ncclSuccess)
                 return cudaErrorUnknown;
             launch_combine(p, ctx->b, ctx->b.gathered, ctx->cfg.world_size, s);
         }
     } else {
-        launch_update(p, ctx->b, false, s);
+        launch_softmin(p, ctx->b, false, s);
+        mark(4);
     }
     mark(5);
     return cudaGetLastError();
@@ -523,7 +529,7 @@ mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, u
     return run_step(ctx, x0, goal, step_index, false, 1);
 }
 
-int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 2 + 4 * ctx->cfg.T : 0; }
+int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 3 + 4 * ctx->cfg.T : 0; }
 
 const float* mppi_get_record_device(const mppi_ctx* ctx) { return ctx ? ctx->b.record : nullptr; }
 
@@ -571,6 +577,7 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
         case MPPI_DBG_NOISE: src = ctx->b.noise; need = 16 * states; break;
         case MPPI_DBG_TERMS: src = ctx->b.terms; need = 4 * states; break;
         case MPPI_DBG_PARTIAL: src = ctx->b.partial; need = 4 * (size_t)p.n_ctrl * p.K; break;
+        case MPPI_DBG_RECORD: src = ctx->b.record; need = 4 * (size_t)p.n_ctrl * (3 + 4 * p.T); break;
         default: return fail(MPPI_ERR_INVALID, "bad debug id");
     }
     if (!host_dst || bytes < need) return fail(MPPI_ERR_INVALID, "destination too small");
@@ -622,8 +629,8 @@ int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
 
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
     if (!ctx) return 0;
-    // noise+shift, rollout, mlp, cost+min, update (+ combine when sharded with NCCL)
-    return 5 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
+    // noise+shift, rollout, mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL)
+    return 4 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
 }
 
 }  // extern "C"

@@ -46,9 +46,10 @@ struct Buffers {
     float* terms;         // [n_ctrl*T*K] SDF-dependent stage cost
     float* partial;       // [n_ctrl*K] non-SDF cost sums
     float* J;             // [n_ctrl*K]
-    unsigned* jmin_bits;  // [n_ctrl] order-preserving encoding of min J
-    float* record;        // [n_ctrl][2 + 4T]  (m_r, S_r, V_r)
-    float* gathered;      // [world][n_ctrl][2 + 4T]
+    unsigned* tickets;    // [n_ctrl] blocks of k_softmin done this step (reset by the last block)
+    float* blkrec;        // [n_ctrl][softmin blocks][3 + 4T] per-block records (m_b, S_b, S2_b, V_b)
+    float* record;        // [n_ctrl][3 + 4T]  this rank's record (m_r, S_r, S2_r, V_r)
+    float* gathered;      // [world][n_ctrl][3 + 4T]
     float* diag;          // [n_ctrl][4]
     int* flags;           // [n_ctrl]
 };
@@ -58,8 +59,8 @@ void launch_noise_shift(const Params& p, const Buffers& b, bool gen_noise, cudaS
 void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s);
 void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s);
-void launch_cost_min(const Params& p, const Buffers& b, cudaStream_t s);
-void launch_update(const Params& p, const Buffers& b, bool write_record, cudaStream_t s);
+void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s);
+int softmin_blocks(int K);
 void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s);
 void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_count, cudaStream_t s);
 

@@ -45,7 +45,7 @@ def timing(name, steps=20):
     torch.cuda.synchronize()
     dt = (time.time() - t0) / steps
     kt = np.median(np.array(st), 0)
-    print(f"timing {name}: wall {dt * 1e3:.3f} ms/step; stages ms (noise, rollout, mlp, cost, update) {kt}", flush=True)
+    print(f"timing {name}: wall {dt * 1e3:.3f} ms/step; stages ms (noise, rollout, mlp, softmin, exchange) {kt}", flush=True)
 
 
 if __name__ == "__main__":
