@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     __shared__ bool s_last;
     const int bb = blockIdx.y, nblk = gridDim.x;
     const int k = blockIdx.x * kSoftminBlock + threadIdx.x;
-    const int W = 3 + 4 * p.T;
+    const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
     // ---- phase 1: thread per sample
     float J = INFINITY;
     if (k < p.K) {
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     const float S = block_reduce(w, red, false);
     const float S2 = block_reduce(w * w, red, false);
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
-    if (threadIdx.x == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; }
+    if (threadIdx.x == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = 0.f; }
     // ---- phase 2: thread per time step, sequential over the block's samples (deterministic)
     const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
     const long long NK = (long long)p.n_ctrl * p.K;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
                 v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
                 v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
             }
-        reinterpret_cast<float4*>(rec + 3)[t] = make_float4(v0, v1, v2, v3);
+        reinterpret_cast<float4*>(rec + 4)[t] = make_float4(v0, v1, v2, v3);
     }
     // ---- last block of this controller combines the block records in order
     __threadfence();
@@ -337,12 +337,12 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
                 const float mi = __ldcg(r);
                 if (!(mi < INFINITY)) continue;
                 const float f = expf((mg - mi) * p.inv_lambda);
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(r + 3) + t);
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(r + 4) + t);
                 V.x = fmaf(v.x, f, V.x); V.y = fmaf(v.y, f, V.y); V.z = fmaf(v.z, f, V.z); V.w = fmaf(v.w, f, V.w);
             }
         if (write_record) {
             float* out = b.record + (long long)bb * W;
-            reinterpret_cast<float4*>(out + 3)[t] = V;
+            reinterpret_cast<float4*>(out + 4)[t] = V;
         } else {
             const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
             float4 Un = U;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     if (threadIdx.x == 0) {
         if (write_record) {
             float* out = b.record + (long long)bb * W;
-            out[0] = mg; out[1] = Sg; out[2] = S2g;
+            out[0] = mg; out[1] = Sg; out[2] = S2g; out[3] = 0.f;
         } else {
             float* d = b.diag + bb * 4;
             d[0] = mg;
@@ -382,7 +382,7 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n_ctrl * p.T) return;
     const int bb = i / p.T, t = i % p.T;
-    const int W = 3 + 4 * p.T;
+    const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
     float m = INFINITY;
     for (int r = 0; r < R; ++r) m = fminf(m, recs[((long long)r * p.n_ctrl + bb) * W]);
     const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
@@ -395,7 +395,7 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
             const float f = expf((m - rec[0]) * p.inv_lambda);
             S += rec[1] * f;
             S2 += rec[2] * f * f;
-            for (int c = 0; c < 4; ++c) v[c] += rec[3 + 4 * t + c] * f;
+            for (int c = 0; c < 4; ++c) v[c] += rec[4 + 4 * t + c] * f;
         }
         if (S > 0.f) {
             Un.x = U.x + v[0] / S; Un.y = U.y + v[1] / S; Un.z = U.z + v[2] / S; Un.w = U.w + v[3] / S;
