@@ -117,9 +117,9 @@ mppi_status mppi_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_
 mppi_status mppi_step_device(mppi_ctx* ctx, const float* d_x0, const float* d_goal, uint64_t step_index);
 
 /* Split-phase sharded step (configs[3] without an NCCL communicator, e.g. emulated ranks):
- * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, S2_r, V_r[T][4]) per
+ * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, S2_r, 0, V_r[T][4]) per
  * controller (S2 = sum of squared weights, for the ESS diagnostic); mppi_record_size() is the record
- * length in floats per controller (3 + 4T); mppi_get_record_device()
+ * length in floats per controller (4 + 4T); mppi_get_record_device()
  * returns the device pointer of [n_ctrl][record]; mppi_step_finish combines R gathered records
  * (device [R][n_ctrl][record], rank order) into U*. */
 mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step_index);
@@ -139,7 +139,7 @@ mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out);
  * MPPI_DBG_QUERIES: [n_ctrl][T][K][rps][4] query rows (p_c, |v|) / (p_c + h d, 0), rps = 2 if w_guide != 0
  * MPPI_DBG_SDF:     [n_ctrl][T][K][rps] s per row     MPPI_DBG_COSTS: [n_ctrl][K] J
  * MPPI_DBG_NOISE:   [T][n_ctrl*K][4] standard normals used   MPPI_DBG_TERMS: [n_ctrl][T][K] SDF stage terms
- * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums   MPPI_DBG_RECORD: [n_ctrl][3 + 4T] this rank's record */
+ * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums   MPPI_DBG_RECORD: [n_ctrl][4 + 4T] this rank's record */
 enum { MPPI_DBG_QUERIES = 0, MPPI_DBG_SDF = 1, MPPI_DBG_COSTS = 2, MPPI_DBG_NOISE = 3, MPPI_DBG_TERMS = 4,
        MPPI_DBG_PARTIAL = 5, MPPI_DBG_RECORD = 6 };
 mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes);

@@ -143,7 +143,7 @@ class Controller:
     def debug(self, what: str) -> np.ndarray:
         n, K, T, r = self.n, self.K, self.T, self.rps
         shapes = {"queries": (n, T, K, r, 4), "sdf": (n, T, K, r), "costs": (n, K), "noise": (T, n * K, 4),
-                  "terms": (n, T, K), "partial": (n, K), "record": (n, 3 + 4 * T)}
+                  "terms": (n, T, K), "partial": (n, K), "record": (n, 4 + 4 * T)}
         out = np.zeros(shapes[what], np.float32)
         _lib._check(self.lib.mppi_debug_copy(self.ctx, DBG[what], _lib._ptr(out), out.nbytes))
         return out

@@ -288,24 +288,33 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     const float S2 = block_reduce(w * w, red, false);
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
     if (threadIdx.x == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = 0.f; }
-    // ---- phase 2: thread per time step, sequential over the block's samples (deterministic)
+    // ---- phase 2: warp per time step (coalesced over the block's samples), fixed shuffle tree
     const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
     const long long NK = (long long)p.n_ctrl * p.K;
-    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int t = warp; t < p.T; t += nw) {
         const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-        if (m < INFINITY)
-            for (int i = 0; i < kn; ++i) {
+        if (m < INFINITY) {
+#pragma unroll 4
+            for (int i = lane; i < kn; i += 32) {
                 const float wi = s_w[i];
-                if (wi == 0.f) continue;
                 const float4 n = nz[i];
                 v0 = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v0);
                 v1 = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v1);
                 v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
                 v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
             }
-        reinterpret_cast<float4*>(rec + 4)[t] = make_float4(v0, v1, v2, v3);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_xor_sync(0xFFFFFFFFu, v0, o);
+            v1 += __shfl_xor_sync(0xFFFFFFFFu, v1, o);
+            v2 += __shfl_xor_sync(0xFFFFFFFFu, v2, o);
+            v3 += __shfl_xor_sync(0xFFFFFFFFu, v3, o);
+        }
+        if (lane == 0) reinterpret_cast<float4*>(rec + 4)[t] = make_float4(v0, v1, v2, v3);
     }
     // ---- last block of this controller combines the block records in order
     __threadfence();
@@ -315,41 +324,39 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     if (!s_last) return;
     __threadfence();
     const float* recs = b.blkrec + (long long)bb * nblk * W;
-    float mg = INFINITY;
-    for (int i = 0; i < nblk; ++i) mg = fminf(mg, __ldcg(recs + (long long)i * W));
+    __shared__ float s_f[kSoftminBlock];   // per-record scale exp((m - m_b)/lambda), nblk <= blocks handled below
+    // global min over block records (thread i reads record i; tree with fixed shape)
+    float mi_loc = INFINITY;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) mi_loc = fminf(mi_loc, __ldcg(recs + (long long)i * W));
+    const float mg = block_reduce(mi_loc, red, true);
     const bool ok = mg < INFINITY;
-    // S, S2 (thread 0 reads them back; the combine order is fixed)
-    float Sg = 0.f, S2g = 0.f;
-    if (ok)
-        for (int i = 0; i < nblk; ++i) {
-            const float* r = recs + (long long)i * W;
-            const float mi = __ldcg(r);
-            if (!(mi < INFINITY)) continue;
-            const float f = expf((mg - mi) * p.inv_lambda);
-            Sg += __ldcg(r + 1) * f;
-            S2g += __ldcg(r + 2) * f * f;
-        }
-    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
-        float4 V = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ok)
+    float sl = 0.f, s2l = 0.f;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+        const float* r = recs + (long long)i * W;
+        const float mi = __ldcg(r);
+        const float f = (ok && mi < INFINITY) ? expf((mg - mi) * p.inv_lambda) : 0.f;
+        if (i < kSoftminBlock) s_f[i] = f;
+        sl += __ldcg(r + 1) * f;
+        s2l += __ldcg(r + 2) * f * f;
+    }
+    const float Sg = block_reduce(sl, red, false);
+    const float S2g = block_reduce(s2l, red, false);
+    for (int tc = threadIdx.x; tc < 4 * p.T; tc += blockDim.x) {
+        float V = 0.f;
+        if (ok) {
+#pragma unroll 8
             for (int i = 0; i < nblk; ++i) {
-                const float* r = recs + (long long)i * W;
-                const float mi = __ldcg(r);
-                if (!(mi < INFINITY)) continue;
-                const float f = expf((mg - mi) * p.inv_lambda);
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(r + 4) + t);
-                V.x = fmaf(v.x, f, V.x); V.y = fmaf(v.y, f, V.y); V.z = fmaf(v.z, f, V.z); V.w = fmaf(v.w, f, V.w);
+                const float f = i < kSoftminBlock ? s_f[i]
+                                                  : expf((mg - __ldcg(recs + (long long)i * W)) * p.inv_lambda);
+                V = fmaf(__ldcg(recs + (long long)i * W + 4 + tc), f, V);
             }
+        }
+        const int t = tc >> 2, c = tc & 3;
         if (write_record) {
-            float* out = b.record + (long long)bb * W;
-            reinterpret_cast<float4*>(out + 4)[t] = V;
+            b.record[(long long)bb * W + 4 + tc] = V;
         } else {
-            const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
-            float4 Un = U;
-            if (ok && Sg > 0.f) {
-                Un.x = U.x + V.x / Sg; Un.y = U.y + V.y / Sg; Un.z = U.z + V.z / Sg; Un.w = U.w + V.w / Sg;
-            }
-            reinterpret_cast<float4*>(b.U_out)[(long long)bb * p.T + t] = Un;
+            const float Uv = b.U_nom[((long long)bb * p.T + t) * 4 + c];
+            b.U_out[((long long)bb * p.T + t) * 4 + c] = (ok && Sg > 0.f) ? Uv + V / Sg : Uv;
         }
     }
     if (threadIdx.x == 0) {

@@ -43,7 +43,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     const size_t Ld = (size_t)c->latent_dim, G = (size_t)(c->n_hidden - 1);
     const size_t rps = c->w_guide != 0.f ? 2 : 1;
     const size_t world = (size_t)(c->world_size > 0 ? c->world_size : 1);
-    const size_t recw = 3 + 4 * T;
+    const size_t recw = 4 + 4 * T;
     size_t sz[B_COUNT];
     sz[B_W1P] = 16 * H;
     sz[B_W1Z] = 4 * H * Ld;
@@ -446,7 +446,7 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
         launch_softmin(p, ctx->b, true, s);
         mark(4);
         if (mode == 0) {
-            const size_t recn = (size_t)p.n_ctrl * (3 + 4 * p.T);
+            const size_t recn = (size_t)p.n_ctrl * (4 + 4 * p.T);
             if (ncclAllGather(ctx->b.record, ctx->b.gathered, recn, ncclFloat, ctx->comm, s) != ncclSuccess)
                 return cudaErrorUnknown;
             launch_combine(p, ctx->b, ctx->b.gathered, ctx->cfg.world_size, s);
@@ -529,7 +529,7 @@ mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, u
     return run_step(ctx, x0, goal, step_index, false, 1);
 }
 
-int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 3 + 4 * ctx->cfg.T : 0; }
+int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 4 + 4 * ctx->cfg.T : 0; }
 
 const float* mppi_get_record_device(const mppi_ctx* ctx) { return ctx ? ctx->b.record : nullptr; }
 
@@ -577,7 +577,7 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
         case MPPI_DBG_NOISE: src = ctx->b.noise; need = 16 * states; break;
         case MPPI_DBG_TERMS: src = ctx->b.terms; need = 4 * states; break;
         case MPPI_DBG_PARTIAL: src = ctx->b.partial; need = 4 * (size_t)p.n_ctrl * p.K; break;
-        case MPPI_DBG_RECORD: src = ctx->b.record; need = 4 * (size_t)p.n_ctrl * (3 + 4 * p.T); break;
+        case MPPI_DBG_RECORD: src = ctx->b.record; need = 4 * (size_t)p.n_ctrl * (4 + 4 * p.T); break;
         default: return fail(MPPI_ERR_INVALID, "bad debug id");
     }
     if (!host_dst || bytes < need) return fail(MPPI_ERR_INVALID, "destination too small");

@@ -47,9 +47,9 @@ struct Buffers {
     float* partial;       // [n_ctrl*K] non-SDF cost sums
     float* J;             // [n_ctrl*K]
     unsigned* tickets;    // [n_ctrl] blocks of k_softmin done this step (reset by the last block)
-    float* blkrec;        // [n_ctrl][softmin blocks][3 + 4T] per-block records (m_b, S_b, S2_b, V_b)
-    float* record;        // [n_ctrl][3 + 4T]  this rank's record (m_r, S_r, S2_r, V_r)
-    float* gathered;      // [world][n_ctrl][3 + 4T]
+    float* blkrec;        // [n_ctrl][softmin blocks][4 + 4T] per-block records (m_b, S_b, S2_b, 0, V_b)
+    float* record;        // [n_ctrl][4 + 4T]  this rank's record (m_r, S_r, S2_r, 0, V_r)
+    float* gathered;      // [world][n_ctrl][4 + 4T]
     float* diag;          // [n_ctrl][4]
     int* flags;           // [n_ctrl]
 };
