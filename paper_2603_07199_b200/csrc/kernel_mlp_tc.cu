@@ -26,6 +26,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/mppi.h"
@@ -590,30 +592,41 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
                      float* sdf_out, bool states_mode, cudaStream_t s) {
     using C = Cfg<H, G>;
     static bool attr_set = false;
-    static int n_sm = 0;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        attr_set = true;
-    }
-    const long long tiles = (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
-    if (tiles == 0) return cudaSuccess;
-    const long long groups = tiles < n_sm / C::CG ? tiles : n_sm / C::CG;
+    static int max_groups = 0;   // co-resident CTA groups (clusters) on this device: the persistent grid
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(groups * C::CG));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = C::CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        int dev, n_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        max_groups = n_sm / C::CG;
+        // with clusters, GPC/TPC floor-sweeping can leave fewer pairs co-resident than SMs/2: a static
+        // round-robin over more groups than fit would serialise a second wave
+        int clusters = 0;
+        cfg.gridDim = dim3((unsigned)(max_groups * C::CG));
+        if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT>, &cfg) == cudaSuccess && clusters > 0)
+            max_groups = clusters < max_groups ? clusters : max_groups;
+        cudaGetLastError();
+        attr_set = true;
+        if (getenv("MPPI_VERBOSE"))
+            fprintf(stderr, "[mppi] k_mlp_tc<%d,%d,%d>: %d SMs, %d co-resident groups of %d CTAs, smem %d B\n", H, G, ACT,
+                    n_sm, max_groups, C::CG, C::SMEM);
+    }
+    const long long tiles = (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
+    if (tiles == 0) return cudaSuccess;
+    const long long groups = tiles < max_groups ? tiles : max_groups;
+    cfg.gridDim = dim3((unsigned)(groups * C::CG));
     return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
                               (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,
                               (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms);
