@@ -91,7 +91,9 @@ __device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, fl
     xd[9] = 0.5f * (qw * wz + qx * wy - qy * wx);
 }
 
-__global__ void __launch_bounds__(128) k_rollout(Params p, Buffers b) {
+constexpr int kRolloutBlock = 64;   // small blocks: K/64 blocks spread the latency-bound rollout over all SMs
+
+__global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) {
     const int bb = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= p.K) return;
@@ -110,9 +112,16 @@ __global__ void __launch_bounds__(128) k_rollout(Params p, Buffers b) {
     const long long col = (long long)bb * p.K + k;
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity;
     float part = 0.f;
+    // software pipelining: the noise / nominal of step t+1 are loaded while step t integrates
+    float4 n_next = b.noise[col];
+    float4 U_next = Un[0];
     for (int t = 0; t < p.T; ++t) {
-        const float4 n = b.noise[(long long)t * NK + col];
-        const float4 U = Un[t];
+        const float4 n = n_next;
+        const float4 U = U_next;
+        if (t + 1 < p.T) {
+            n_next = b.noise[(long long)(t + 1) * NK + col];
+            U_next = Un[t + 1];
+        }
         const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
         const float u1 = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
         const float u2 = clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]);
@@ -157,8 +166,8 @@ __global__ void __launch_bounds__(128) k_rollout(Params p, Buffers b) {
 }
 
 void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s) {
-    dim3 grid((p.K + 127) / 128, p.n_ctrl);
-    k_rollout<<<grid, 128, 0, s>>>(p, b);
+    dim3 grid((p.K + kRolloutBlock - 1) / kRolloutBlock, p.n_ctrl);
+    k_rollout<<<grid, kRolloutBlock, 0, s>>>(p, b);
 }
 
 // ------------------------------------------------------------------ K2f: fp32 SDF-MLP on CUDA cores
@@ -248,7 +257,7 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 // records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
 // U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
-constexpr int kSoftminBlock = 256;
+constexpr int kSoftminBlock = 128;
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
     #pragma unroll
