@@ -257,7 +257,7 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 // records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
 // U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
-constexpr int kSoftminBlock = 128;
+constexpr int kSoftminBlock = 256;
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
     #pragma unroll
