@@ -182,34 +182,29 @@ def main():
     cfg = pick_config(args.config, world)
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
-    # ---- shard (configs[3]: samples; configs[4]: controllers; others: replicas only)
-    K_global, k_offset, n_ctrl = cfg.K, 0, cfg.n_ctrl
+    # ---- shard (configs[3]: samples + one NCCL all-gather; configs[4]: controllers; others: replicas)
+    from paper_2603_07199_b200 import shard
+    plan = shard.plan(cfg, world, rank)
+    sharded = plan.sharded
     nccl_id = None
-    sharded = world > 1 and cfg.name in ("c3",)
     if sharded:
-        assert cfg.K % world == 0
-        K_local = cfg.K // world
-        k_offset = rank * K_local
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    else:
-        K_local = cfg.K
-        if world > 1 and cfg.name == "c4":
-            n_ctrl = cfg.n_ctrl // world
-    lcfg = cfg.replace(K=K_local, n_ctrl=n_ctrl)
+    lcfg = cfg.replace(K=plan.K_local, n_ctrl=plan.n_ctrl_local)
     ctrl = Controller(lcfg, device=local, noise_mode="device", world_size=world if sharded else 1,
-                      rank=rank if sharded else 0, K_global=K_global, k_offset=k_offset, nccl_id=nccl_id)
+                      rank=rank if sharded else 0, K_global=plan.K_global, k_offset=plan.k_offset, nccl_id=nccl_id)
     Ws, bs = synth.make_weights(cfg)
     ctrl.set_sdf_weights(Ws, bs)
-    Tq = synth.make_query_transforms(lcfg)
-    ctrl.set_latent(synth.make_latents(lcfg), Tq)
-    ctrl.set_nominal(synth.make_nominal(lcfg))
-    x0_h, goal_h = synth.make_x0(lcfg), synth.make_goals(lcfg)
+    csl = slice(plan.ctrl_offset, plan.ctrl_offset + plan.n_ctrl_local)
+    Tq = synth.make_query_transforms(cfg)[csl]
+    ctrl.set_latent(synth.make_latents(cfg)[csl], Tq)
+    ctrl.set_nominal(synth.make_nominal(cfg)[csl])
+    x0_h, goal_h = synth.make_x0(cfg)[csl], synth.make_goals(cfg)[csl]
     dev = torch.device("cuda", local)
     x0_d = torch.from_numpy(x0_h).to(dev)
     goal_d = torch.from_numpy(goal_h).to(dev)
-    latents = [synth.make_latents(lcfg, frame=f) for f in range(1 + (args.warmup + args.steps) // 5)]
+    latents = [synth.make_latents(cfg, frame=f)[csl] for f in range(1 + (args.warmup + 2 * args.warmup + args.steps) // 5 + 1)]
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     ctrl.set_profiling(True)
@@ -250,7 +245,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    units_per_step = cfg.n_ctrl * cfg.K * cfg.T            # rollout-steps of the whole job (all ranks)
+    # rollout-steps of the whole job (all ranks); replicas each run the full configuration
+    units_per_step = cfg.n_ctrl * cfg.K * cfg.T * (world if plan.mode == "replica" else 1)
     value = units_per_step * args.steps / (total_ms * 1e-3)
 
     # ---- end to end through the public API with host buffers (pinned staging H2D, D2H of U*)
@@ -288,14 +284,15 @@ def main():
                 "stage_ms": {k: float(v) for k, v in zip(["noise_shift", "rollout", "sdf_mlp", "softmin_update", "exchange"], kt)}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if sharded or cfg.name == "c4" else "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong" if plan.mode != "replica" else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded; random Kaiming-uniform MLP weights, N(0,1) latents)",
             "config": {"workload": workload_name(cfg, world), "n_ctrl": cfg.n_ctrl, "K": cfg.K, "T": cfg.T,
                        "per_rank": {"n_ctrl": lcfg.n_ctrl, "K": lcfg.K},
                        "l2": "flushed (256 MiB write) before every timed step, outside its events",
                        "latent": "redrawn every 5 steps between timed steps (per-frame fold, off the iteration)",
-                       "parallelism": f"samples sharded x{world} + NCCL all-gather" if sharded else
-                       (f"controllers x{world}" if world > 1 else "single GPU")},
+                       "parallelism": {"samples": f"samples sharded x{world} + NCCL all-gather of the softmin record",
+                                       "controllers": f"controllers x{world}, no communication",
+                                       "replica": "single GPU" if world == 1 else f"{world} independent replicas"}[plan.mode]},
             "latency_ms": {"mean": ms_per_step, "median": float(np.median(step_ms)),
                            "p99": float(np.percentile(step_ms, 99))},
             "roofline": roofline,
