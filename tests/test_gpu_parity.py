@@ -314,3 +314,43 @@ def test_sharded_ranks_match_unsharded_oracle(R):
     c1.set_nominal(U)
     c1.step(x0, goal, 0)
     np.testing.assert_allclose(c1.get_controls()[0], outs[0], atol=1e-4)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_full_size_sampled_parity(name):
+    """BASELINE configs[1..4] at full size with device noise (the bench's launch configuration): the
+    oracle recomputes sampled rollouts one by one (global Philox counters) and their SDF rows and
+    costs are compared; the whole update is checked by the softmin property on the GPU's own costs."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config(name)
+    Ws, bs = synth.make_weights(cfg)
+    z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
+                          synth.make_goals(cfg), synth.make_nominal(cfg))
+    ctrl = Controller(cfg, noise_mode="device")
+    ctrl.set_sdf_weights(Ws, bs)
+    ctrl.set_latent(z, Tq)
+    ctrl.set_nominal(U)
+    ctrl.step(x0, goal, 7)
+    Ug, _ = ctrl.get_controls()
+    J = ctrl.debug("costs").astype(np.float64)
+    sdf = ctrl.debug("sdf")
+    q = ctrl.debug("queries")
+    oc = oracle.make_cfg(cfg)
+    rng = np.random.default_rng(1)
+    ctrls = rng.choice(cfg.n_ctrl, size=min(cfg.n_ctrl, 3), replace=False)
+    for b in ctrls:
+        for k in rng.choice(cfg.K, size=6, replace=False):
+            nz = oracle.noise(cfg.seed, 7, int(b) * cfg.K + int(k), 1, cfg.T)[:, 0]
+            r = oracle.rollout(oc, Ws, bs, z[b], Tq[b], x0[b], goal[b], U[b], nz)
+            ref = {"queries": r["queries"][None, None], "sdf": r["sdf"][None, None], "stage": r["stage"][None, None]}
+            ok, err = gh.check_queries(cfg, gh.gpu_queries_like_oracle(q[b:b + 1, :, k:k + 1]), ref["queries"])
+            assert ok, (b, k, err)
+            s = gh.gpu_sdf_like_oracle(sdf[b:b + 1, :, k:k + 1])[0, 0]
+            assert np.abs(s - r["sdf"]).max() <= gh.ABS_SDF_BF16
+            tol = gh.cost_tol(cfg, ref, gh.ABS_SDF_BF16)[0, 0]
+            assert abs(J[b, k] - r["J"]) <= tol, (b, k, J[b, k], r["J"], tol)
+    noise = ctrl.debug("noise").astype(np.float64)
+    for b in ctrls:
+        prop = gh.softmin_property(cfg, U[b], noise[:, b * cfg.K:(b + 1) * cfg.K], J[b])
+        assert np.abs(Ug[b] - prop).max() <= gh.ABS_U
+    ctrl.close()
