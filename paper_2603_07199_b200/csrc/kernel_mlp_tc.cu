@@ -63,7 +63,8 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 constexpr int kEpiWarps = MPPI_EPI_WARPS;   // 8 or 16 (2 or 4 per SMSP)
 constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 weight loader, 2-3 idle
-constexpr int kColGroups = kEpiWarps / 4;   // column groups per TMEM lane quarter
+constexpr int kGroupWarps = kEpiWarps / 2;   // epilogue warps per tile slot (slot-specialised groups)
+constexpr int kColGroups = kGroupWarps / 4; // column groups per TMEM lane quarter within a group
 constexpr int kCW = 16;         // TMEM columns per epilogue load (register budget: 96/thread)
 constexpr int kTileRows = 128;
 
@@ -237,7 +238,7 @@ struct Cfg {
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
-    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 slots][H] float4 (W1p, b1'), scaled
+    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 groups][H] float4 (W1p, b1'), scaled
     static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 slots][col groups][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * 2 * kColGroups * kTileRows;  // [4 bufs][128] float4 query rows
     static constexpr int OFF_BAR = OFF_ROWS + 4 * 16 * kTileRows;
@@ -283,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
     for (int i = threadIdx.x; i < H; i += kThreads) s_wo[i] = w_out[i];
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_AREADY + i), kEpiWarps * CG);
-        for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kEpiWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
+        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_AREADY + i), kGroupWarps * CG);
+        for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kGroupWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
         for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_ROWS + i), 1);
@@ -357,27 +358,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ================= epilogue (16 warps per CTA)
+        // ================= epilogue: two groups of kGroupWarps warps, group sl owns TMEM slot sl and the
+        // CTA's tiles i = sl, sl + 2, ... (one group computes while the other waits for its MMA unit)
         const int e = warp - kEpiWarp0;
-        const int g = warp & 3;            // TMEM lane quarter
-        const int cgi = e >> 2;            // column group of each N-half (QW columns)
+        const int sl = e / kGroupWarps;            // tile slot of this group
+        const int eg = e % kGroupWarps;
+        const int g = warp & 3;                    // TMEM lane quarter
+        const int cgi = eg >> 2;                   // column group of each N-half (QW columns)
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
-        const bool tracer = lane == 0 && (e == 0 || e == kEpiWarps - 1);
-        const int trole = 1 + (e == kEpiWarps - 1);
+        const int gthreads = kGroupWarps * 32;
+        const int gtid = eg * 32 + lane;
+        const bool tracer = lane == 0 && eg == 0 && sl < 2;
+        const int trole = 1 + sl;
         const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
-        uint32_t mma_cnt[2] = {0, 0};
-        long long staged_lo = -1;   // controllers staged_lo, staged_lo + 1 have (W1p, b1') in s_w1[0], s_w1[1]
-        auto arrive_sched = [&](int i) {   // epilogue -> MMA issuer (leader CTA)
+        uint32_t mma_cnt = 0;
+        long long staged = -1;                     // controller whose (W1p, b1') sits in this group's s_w1
+        float4* w1g = s_w1 + sl * H;
+        float* part = s_part + sl * kColGroups * kTileRows;
+        auto arrive_sched = [&](int i) {           // epilogue -> MMA issuer (leader CTA)
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(i));
             else mbar_arrive_local(bar(i));
         };
         auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
         // query rows of this CTA's part of tile i -> smem buffer i & 3 by one bulk-async copy (TMA engine),
-        // issued two tiles ahead by one elected epilogue thread
+        // issued two tiles (one tile of this slot) ahead by one elected thread of the group
         const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS);
-        const bool row_issuer = e == 0 && lane == 0;
+        const bool row_issuer = eg == 0 && lane == 0;
         auto issue_rows = [&](long long i) {
             if (!row_issuer || i >= n_my) return;
             const long long r0 = tile_row0(tile_of(i));
@@ -394,34 +402,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long row = tile_row0(tile_of(i)) + row_in_tile;
             return row < n_rows ? s_rows[(i & 3) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
         };
-        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of slot sl, for tile index i
-        auto layer1 = [&](long long i, int sl) {
+        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of this slot, for tile index i
+        auto layer1 = [&](long long i) {
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
             mbar_wait(bar(BAR_ROWS + (int)(i & 3)), (uint32_t)((i >> 2) & 1));
             const float4 q = row_of(i);
-            issue_rows(i + 2);   // buffer (i+2)&3 was last read by tile i-2's layer 1 (behind bar 1)
+            issue_rows(i + 2);   // buffer (i+2)&3 was last read by tile i-2 (this group, behind its bar)
             const long long row0 = tile_row0(t1);
-            const long long rlast = min(row0 + kTileRows, n_rows) - 1;
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
-            const long long hi = states_mode ? rlast / rows_per_ctrl : ctrl_fixed;
-            if (lo != staged_lo) {   // uniform across the epilogue warps
-                named_bar_sync(2, kEpiWarps * 32);   // nobody still reads the old staging
-                for (int i = threadIdx.x - kEpiWarp0 * 32; i < 2 * H; i += kEpiWarps * 32) {
-                    const long long bb = lo + i / H;
-                    const int j = i % H;
+            if (lo != staged) {   // uniform across the group
+                named_bar_sync(3 + sl, gthreads);   // nobody in the group still reads the old staging
+                for (int j = gtid; j < H; j += gthreads) {
                     const float4 w = w1p[j];
-                    const float bv = bb < p.n_ctrl ? b1f[(size_t)bb * H + j] : 0.f;
-                    s_w1[i] = make_float4(w.x * kP, w.y * kP, w.z * kP, bv * kP);
+                    const float bv = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] : 0.f;
+                    w1g[j] = make_float4(w.x * kP, w.y * kP, w.z * kP, bv * kP);
                 }
-                staged_lo = lo;
-                named_bar_sync(2, kEpiWarps * 32);
+                staged = lo;
+                named_bar_sync(3 + sl, gthreads);
             }
             const long long row = row0 + row_in_tile;
             const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
-            const int slot = (int)min(bb - lo, 1ll);
-            const float4* wrow = s_w1 + slot * H;
-            const float* bfar = (hi - lo > 1 && bb - lo > 1) ? b1f + (size_t)bb * H : nullptr;
+            const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
             const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
             const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
 #pragma unroll
@@ -432,21 +434,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t packed[kCW / 2];
                     if (!any_far) {
 #pragma unroll
-                        for (int i = 0; i < kCW; i += 2) {
-                            const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
+                        for (int i2 = 0; i2 < kCW; i2 += 2) {
+                            const float4 w0 = w1g[j0 + i2], w1 = w1g[j0 + i2 + 1];
                             const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, w0.w)));
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
-                            packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                            packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
                         }
-                    } else {   // rare (K*T < one tile): rows of a third controller in this tile
+                    } else {   // rare: the tile crosses a controller boundary
 #pragma unroll
-                        for (int i = 0; i < kCW; i += 2) {
-                            const float4 w0 = wrow[j0 + i], w1 = wrow[j0 + i + 1];
-                            const float b0 = bfar ? __ldg(bfar + j0 + i) * kP : w0.w;
-                            const float b1 = bfar ? __ldg(bfar + j0 + i + 1) * kP : w1.w;
+                        for (int i2 = 0; i2 < kCW; i2 += 2) {
+                            const float4 w0 = w1g[j0 + i2], w1 = w1g[j0 + i2 + 1];
+                            const float b0 = bfar ? __ldg(bfar + j0 + i2) * kP : w0.w;
+                            const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : w1.w;
                             const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, b0)));
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, b1)));
-                            packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                            packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
                         }
                     }
                     tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
@@ -459,118 +461,105 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
-        issue_rows(0);
-        issue_rows(1);
-        for (int sl = 0; sl < 2; ++sl)
-            if (sl < n_my) layer1(sl, sl);
-        for (long long i0 = 0; i0 < n_my; i0 += 2) {
-            const int ns = i0 + 1 < n_my ? 2 : 1;
-            uint32_t keep[2][C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
-            float sdot[2] = {0.f, 0.f};
+        issue_rows(sl);
+        if (sl < n_my) layer1(sl);
+        for (long long i = sl; i < n_my; i += 2) {
+            uint32_t keep[C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
+            float sdot = 0.f;
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
                 const float* hb = s_hb + l * H;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    if (tracer) TC_TRACE(trole, 3, l, h, sl, i);
+                    mbar_wait(bar(BAR_MMA + sl), (mma_cnt++) & 1);
+                    tc_fence_after();
+                    if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
+                    const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
+                    const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
 #pragma unroll
-                    for (int sl = 0; sl < 2; ++sl) {
-                        if (sl >= ns) continue;
-                        if (tracer) TC_TRACE(trole, 3, l, h, sl, i0);
-                        mbar_wait(bar(BAR_MMA + sl), (mma_cnt[sl]++) & 1);
-                        tc_fence_after();
-                        if (tracer) TC_TRACE(trole, 4, l, h, sl, i0);
-                        const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
-                        const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
-                        // one 16-column TMEM chunk at a time (register budget); D of the slot is released
-                        // after the last chunk's load: the other slot's MMA unit (~1k cycles) covers it.
-#pragma unroll
-                        for (int k = 0; k < C::NCH; ++k) {
-                            uint32_t acc[kCW];
-                            tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
-                            tmem_wait_ld();
-                            if (k == C::NCH - 1) {
-                                tc_fence_before();
-                                __syncwarp();
-                                if (lane == 0) arrive_sched(BAR_DFREE + sl);
-                                if (tracer) TC_TRACE(trole, 10, l, h, sl, i0);
-                            }
-                            const int j0 = h * C::HALF + cgi * C::QW + k * kCW;   // output neuron index
-                            if (!last) {
-                                uint32_t packed[kCW / 2];
-#pragma unroll
-                                for (int i = 0; i < kCW; i += 4) {
-                                    const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
-                                    const float x0 = fmaf(__uint_as_float(acc[i]), kP, bv.x);
-                                    const float x1 = fmaf(__uint_as_float(acc[i + 1]), kP, bv.y);
-                                    const float x2 = fmaf(__uint_as_float(acc[i + 2]), kP, bv.z);
-                                    const float x3 = fmaf(__uint_as_float(acc[i + 3]), kP, bv.w);
-                                    packed[i / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
-                                    packed[i / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
-                                }
-                                if (h == 0) {
-#pragma unroll
-                                    for (int i = 0; i < kCW / 2; ++i) keep[sl][k * (kCW / 2) + i] = packed[i];
-                                } else {
-                                    // both N-halves of this layer done: A of the slot is dead -> next input
-                                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2),
-                                             &keep[sl][k * (kCW / 2)]);
-                                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
-                                }
-                            } else {
-#pragma unroll
-                                for (int i = 0; i < kCW; i += 4) {
-                                    const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i);
-                                    const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i);
-                                    const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i]), kP, bv.x)),
-                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[i + 1]), kP, bv.y)));
-                                    const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i + 2]), kP, bv.z)),
-                                                                    act_pre<ACT>(fmaf(__uint_as_float(acc[i + 3]), kP, bv.w)));
-                                    sdot[sl] = fmaf(__uint_as_float(p0 << 16), wv.x, sdot[sl]);
-                                    sdot[sl] = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot[sl]);
-                                    sdot[sl] = fmaf(__uint_as_float(p1 << 16), wv.z, sdot[sl]);
-                                    sdot[sl] = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot[sl]);
-                                }
-                            }
-                        }
-                        if (!last && h == 1) {
-                            tmem_wait_st();
+                    for (int k = 0; k < C::NCH; ++k) {
+                        uint32_t acc[kCW];
+                        tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
+                        tmem_wait_ld();
+                        if (k == C::NCH - 1) {   // D of the slot may be overwritten now
                             tc_fence_before();
                             __syncwarp();
-                            if (lane == 0) arrive_sched(BAR_AREADY + sl);
+                            if (lane == 0) arrive_sched(BAR_DFREE + sl);
+                            if (tracer) TC_TRACE(trole, 10, l, h, sl, i);
                         }
-                        if (tracer) TC_TRACE(trole, 5, l, h, sl, i0);
-                        if (last && h == 1) {
-                            // ---- output of this slot's tile: combine column groups, FD pair, write
-                            const long long tile = tile_of(i0 + sl);
-                            float* part = s_part + sl * kColGroups * kTileRows;
-                            part[cgi * kTileRows + row_in_tile] = sdot[sl];
-                            named_bar_sync(1, kEpiWarps * 32);
-                            if (cgi == 0) {
-                                float sv = __ldg(b_out);
+                        const int j0 = h * C::HALF + cgi * C::QW + k * kCW;   // output neuron index
+                        if (!last) {
+                            uint32_t packed[kCW / 2];
 #pragma unroll
-                                for (int q = 0; q < kColGroups; ++q) sv += part[q * kTileRows + row_in_tile];
-                                const long long row = tile_row0(tile) + row_in_tile;
-                                if (row < n_rows && sdf_out) sdf_out[row] = sv;
-                                if (states_mode) {
-                                    if (p.rps == 2) {
-                                        const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
-                                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                                           p.w_guide * row_of(i0 + sl).w * (s1 - sv) * p.inv_fd_h;
-                                        if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
-                                    } else {
-                                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
-                                        if (row < n_rows) terms[row] = term;
-                                    }
-                                }
+                            for (int i2 = 0; i2 < kCW; i2 += 4) {
+                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
+                                const float x0 = fmaf(__uint_as_float(acc[i2]), kP, bv.x);
+                                const float x1 = fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y);
+                                const float x2 = fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z);
+                                const float x3 = fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w);
+                                packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                                packed[i2 / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
                             }
-                            if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i0);
-                            // next tile of this slot: its layer 1 overlaps the other slot's last MMAs
-                            if (i0 + 2 + sl < n_my) layer1(i0 + 2 + sl, sl);
+                            if (h == 0) {
+#pragma unroll
+                                for (int i2 = 0; i2 < kCW / 2; ++i2) keep[k * (kCW / 2) + i2] = packed[i2];
+                            } else {
+                                // both N-halves of this layer done: A of the slot is dead -> next input
+                                tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2), &keep[k * (kCW / 2)]);
+                                tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                            }
+                        } else {
+#pragma unroll
+                            for (int i2 = 0; i2 < kCW; i2 += 4) {
+                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
+                                const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i2);
+                                const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i2]), kP, bv.x)),
+                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y)));
+                                const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z)),
+                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w)));
+                                sdot = fmaf(__uint_as_float(p0 << 16), wv.x, sdot);
+                                sdot = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot);
+                                sdot = fmaf(__uint_as_float(p1 << 16), wv.z, sdot);
+                                sdot = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot);
+                            }
                         }
+                    }
+                    if (!last && h == 1) {
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_sched(BAR_AREADY + sl);
+                    }
+                    if (tracer) TC_TRACE(trole, 5, l, h, sl, i);
+                }
+            }
+            // ---- output of this tile: combine column groups, FD pair, write
+            const long long tile = tile_of(i);
+            part[cgi * kTileRows + row_in_tile] = sdot;
+            named_bar_sync(1 + sl, gthreads);
+            if (cgi == 0) {
+                float sv = __ldg(b_out);
+#pragma unroll
+                for (int q2 = 0; q2 < kColGroups; ++q2) sv += part[q2 * kTileRows + row_in_tile];
+                const long long row = tile_row0(tile) + row_in_tile;
+                if (row < n_rows && sdf_out) sdf_out[row] = sv;
+                if (states_mode) {
+                    if (p.rps == 2) {
+                        const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
+                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
+                                           p.w_guide * row_of(i).w * (s1 - sv) * p.inv_fd_h;
+                        if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
+                    } else {
+                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
+                        if (row < n_rows) terms[row] = term;
                     }
                 }
             }
+            named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
+            if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
+            if (i + 2 < n_my) layer1(i + 2);   // next tile of this slot; overlaps the other slot's MMAs
         }
     }
     // ---- teardown
