@@ -63,8 +63,6 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 constexpr int kEpiWarps = MPPI_EPI_WARPS;   // 8 or 16 (2 or 4 per SMSP)
 constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 weight loader, 2-3 idle
-constexpr int kGroupWarps = kEpiWarps / 2;   // epilogue warps per tile slot (slot-specialised groups)
-constexpr int kColGroups = kGroupWarps / 4; // column groups per TMEM lane quarter within a group
 constexpr int kCW = 16;         // TMEM columns per epilogue load (register budget: 96/thread)
 constexpr int kTileRows = 128;
 
@@ -230,26 +228,30 @@ struct Cfg {
     static constexpr int ROWS_B = HALF / CG;                 // weight rows (N) of a unit held per CTA
     static constexpr int UNIT_BYTES = ROWS_B * HALF * 2;     // bf16 B block of one unit in one CTA
     static constexpr int W_BYTES = G * 4 * UNIT_BYTES;       // resident weights per CTA
-    static constexpr int TMEM_COLS = 2 * H;                  // two tile slots x (D half + A)
     static constexpr int SLOT_COLS = H;                      // per slot: D [0, HALF) fp32, A [HALF, H) bf16x2
-    static constexpr int QW = HALF / kColGroups;             // epilogue columns per warp per unit
+    static constexpr int NSLOT = 512 / SLOT_COLS;            // tiles in flight per CTA: 2 (H=256), 4 (H=128)
+    static constexpr int TMEM_COLS = NSLOT * SLOT_COLS;      // = 512
+    static constexpr int GW = kEpiWarps / NSLOT;             // epilogue warps per slot group (8 or 4)
+    static constexpr int COLG = GW / 4;                      // column groups per TMEM lane quarter in a group
+    static constexpr int NROWBUF = 2 * NSLOT;                // query-row buffers (prefetch one slot-tile ahead)
+    static constexpr int QW = HALF / COLG;                   // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
-    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [2 groups][H] float4 (W1p, b1'), scaled
-    static constexpr int OFF_PART = OFF_W1 + 2 * 16 * H;             // [2 slots][col groups][128] partial dots
-    static constexpr int OFF_ROWS = OFF_PART + 4 * 2 * kColGroups * kTileRows;  // [4 bufs][128] float4 query rows
-    static constexpr int OFF_BAR = OFF_ROWS + 4 * 16 * kTileRows;
-    static constexpr int OFF_TMEM = OFF_BAR + 8 * 16;
+    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [NSLOT groups][H] float4 (W1p, b1'), scaled
+    static constexpr int OFF_PART = OFF_W1 + NSLOT * 16 * H;         // [NSLOT][COLG][128] partial dots
+    static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
+    static constexpr int OFF_BAR = OFF_ROWS + NROWBUF * 16 * kTileRows;
+    static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
     static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-// Barrier slots (8 B each)
-enum { BAR_AREADY = 0 /*[2 slots]*/, BAR_DFREE = 4 /*[2 slots]*/, BAR_MMA = 6 /*[2 slots]*/, BAR_WLOCAL = 8,
-       BAR_WREADY = 9, BAR_ROWS = 10 /*[4 row buffers]*/ };
+// Barrier slots (8 B each): per tile slot (up to 4) and per query-row buffer (up to 8)
+enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slots]*/, BAR_WLOCAL = 12,
+       BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/ };
 
 template <int H, int G, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -284,11 +286,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
     for (int i = threadIdx.x; i < H; i += kThreads) s_wo[i] = w_out[i];
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_AREADY + i), kGroupWarps * CG);
-        for (int i = 0; i < 2; ++i) { mbar_init(bar(BAR_DFREE + i), kGroupWarps * CG); mbar_init(bar(BAR_MMA + i), 1); }
+        for (int i = 0; i < C::NSLOT; ++i) {
+            mbar_init(bar(BAR_AREADY + i), C::GW * CG);
+            mbar_init(bar(BAR_DFREE + i), C::GW * CG);
+            mbar_init(bar(BAR_MMA + i), 1);
+        }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
-        for (int i = 0; i < 4; ++i) mbar_init(bar(BAR_ROWS + i), 1);
+        for (int i = 0; i < C::NROWBUF; ++i) mbar_init(bar(BAR_ROWS + i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -325,15 +330,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 0) {
         // ================= MMA issuer (one thread of the leader CTA)
-        // Two tiles in flight (TMEM slots 0/1). Per layer and N-half h, one full-K unit per slot, issued
-        // X(h0) Y(h0) X(h1) Y(h1): while the epilogue drains one slot the tensor pipe works on the other.
+        // NSLOT tiles in flight (TMEM slots). Per layer and N-half h, one full-K unit per slot, issued slot by
+        // slot (X(h0) Y(h0) .. X(h1) Y(h1) ..): while the epilogue drains one slot the tensor pipe works on
+        // the others.
         if (lane == 0 && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::HALF);
             const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
-            uint32_t a_cnt[2] = {0, 0}, u_cnt[2] = {0, 0};
+            uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
-            for (long long i0 = 0; i0 < n_my; i0 += 2) {
-                const int ns = i0 + 1 < n_my ? 2 : 1;
+            for (long long i0 = 0; i0 < n_my; i0 += C::NSLOT) {
+                const int ns = (int)min((long long)C::NSLOT, n_my - i0);
                 for (int l = 0; l < G; ++l)
                     for (int h = 0; h < 2; ++h)
                         for (int sl = 0; sl < ns; ++sl) {
@@ -358,18 +364,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ================= epilogue: two groups of kGroupWarps warps, group sl owns TMEM slot sl and the
-        // CTA's tiles i = sl, sl + 2, ... (one group computes while the other waits for its MMA unit)
+        // ================= epilogue: NSLOT groups of GW warps, group sl owns TMEM slot sl and the CTA's
+        // tiles i = sl, sl + NSLOT, ... (one group computes while the others wait for their MMA units)
+        constexpr int kColGroups = C::COLG;
         const int e = warp - kEpiWarp0;
-        const int sl = e / kGroupWarps;            // tile slot of this group
-        const int eg = e % kGroupWarps;
+        const int sl = e / C::GW;                  // tile slot of this group
+        const int eg = e % C::GW;
         const int g = warp & 3;                    // TMEM lane quarter
         const int cgi = eg >> 2;                   // column group of each N-half (QW columns)
         const int row_in_tile = g * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(g * 32) << 16;
-        const int gthreads = kGroupWarps * 32;
+        const int gthreads = C::GW * 32;
         const int gtid = eg * 32 + lane;
-        const bool tracer = lane == 0 && eg == 0 && sl < 2;
+        const bool tracer = lane == 0 && eg == 0 && sl < 2;   // trace roles 1, 2 = slots 0, 1
         const int trole = 1 + sl;
         const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
         uint32_t mma_cnt = 0;
@@ -382,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
-        // query rows of this CTA's part of tile i -> smem buffer i & 3 by one bulk-async copy (TMA engine),
-        // issued two tiles (one tile of this slot) ahead by one elected thread of the group
+        // query rows of this CTA's part of tile i -> smem buffer i % NROWBUF by one bulk-async copy (TMA
+        // engine), issued one tile of this slot (NSLOT tiles) ahead by one elected thread of the group
         const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS);
         const bool row_issuer = eg == 0 && lane == 0;
         auto issue_rows = [&](long long i) {
@@ -391,35 +398,35 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long r0 = tile_row0(tile_of(i));
             const long long nv = min((long long)kTileRows, n_rows - r0);
             if (nv <= 0) {
-                mbar_arrive_local(bar(BAR_ROWS + (int)(i & 3)));
+                mbar_arrive_local(bar(BAR_ROWS + (int)(i % C::NROWBUF)));
                 return;
             }
-            mbar_expect_tx(bar(BAR_ROWS + (int)(i & 3)), (uint32_t)(16 * nv));
-            bulk_g2s(sbase + C::OFF_ROWS + (uint32_t)((i & 3) * 16 * kTileRows), rows + r0, (uint32_t)(16 * nv),
-                     bar(BAR_ROWS + (int)(i & 3)));
+            mbar_expect_tx(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)(16 * nv));
+            bulk_g2s(sbase + C::OFF_ROWS + (uint32_t)((i % C::NROWBUF) * 16 * kTileRows), rows + r0, (uint32_t)(16 * nv),
+                     bar(BAR_ROWS + (int)(i % C::NROWBUF)));
         };
         auto row_of = [&](long long i) {   // this thread's query row of tile i (after its buffer landed)
             const long long row = tile_row0(tile_of(i)) + row_in_tile;
-            return row < n_rows ? s_rows[(i & 3) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
+            return row < n_rows ? s_rows[(i % C::NROWBUF) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of this slot, for tile index i
         auto layer1 = [&](long long i) {
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
-            mbar_wait(bar(BAR_ROWS + (int)(i & 3)), (uint32_t)((i >> 2) & 1));
+            mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
             const float4 q = row_of(i);
-            issue_rows(i + 2);   // buffer (i+2)&3 was last read by tile i-2 (this group, behind its bar)
+            issue_rows(i + C::NSLOT);   // that buffer was last read by tile i - NSLOT (this group, behind its bar)
             const long long row0 = tile_row0(t1);
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             if (lo != staged) {   // uniform across the group
-                named_bar_sync(3 + sl, gthreads);   // nobody in the group still reads the old staging
+                named_bar_sync(1 + C::NSLOT + sl, gthreads);   // nobody in the group still reads the old staging
                 for (int j = gtid; j < H; j += gthreads) {
                     const float4 w = w1p[j];
                     const float bv = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] : 0.f;
                     w1g[j] = make_float4(w.x * kP, w.y * kP, w.z * kP, bv * kP);
                 }
                 staged = lo;
-                named_bar_sync(3 + sl, gthreads);
+                named_bar_sync(1 + C::NSLOT + sl, gthreads);
             }
             const long long row = row0 + row_in_tile;
             const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         issue_rows(sl);
         if (sl < n_my) layer1(sl);
-        for (long long i = sl; i < n_my; i += 2) {
+        for (long long i = sl; i < n_my; i += C::NSLOT) {
             uint32_t keep[C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
             float sdot = 0.f;
 #pragma unroll 1
@@ -559,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
-            if (i + 2 < n_my) layer1(i + 2);   // next tile of this slot; overlaps the other slot's MMAs
+            if (i + C::NSLOT < n_my) layer1(i + C::NSLOT);   // next tile of this slot; overlaps the others' MMAs
         }
     }
     // ---- teardown
