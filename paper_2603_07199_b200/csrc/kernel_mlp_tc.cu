@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
             mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
+            if (tracer) TC_TRACE(trole, 11, 0, 0, sl, t1);
             const float4 q = row_of(i);
             issue_rows(i + C::NSLOT);   // that buffer was last read by tile i - NSLOT (this group, behind its bar)
             const long long row0 = tile_row0(t1);
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                 }
             }
+            if (tracer) TC_TRACE(trole, 12, 0, 0, sl, t1);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();

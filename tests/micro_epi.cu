@@ -21,6 +21,8 @@ __device__ __forceinline__ uint32_t pack(float a, float b) {
 // 4: silu + pack + unpack/dot (last layer); 5: F2F-free pack via PRMT of truncated halves (lower bound)
 template <int MODE>
 __global__ void k(uint32_t* out, long long* cyc, float b) {
+    __shared__ float4 sw[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sw[i] = make_float4(0.01f * i, 0.02f, 0.03f, 0.5f);
     float v[NI];
     uint32_t acc = 0;
     float dot = 0.f;
@@ -54,12 +56,18 @@ __global__ void k(uint32_t* out, long long* cyc, float b) {
                 acc ^= pack(fmaxf(x0 + b, 0.f), fmaxf(x1 + b, 0.f));
                 v[i] = x0 * 0.999f;
                 v[i + 1] = x1 * 0.999f;
-            } else {
+            } else if constexpr (MODE == 5) {
                 float h0 = fmaf(x0, 0.5f, b), h1 = fmaf(x1, 0.5f, b);
                 const float y0 = fmaf(h0, tanh_a(h0), h0), y1 = fmaf(h1, tanh_a(h1), h1);
                 acc ^= __byte_perm(__float_as_uint(y0), __float_as_uint(y1), 0x7632);
                 v[i] = h0 + 1.0f;
                 v[i + 1] = h1 + 1.0f;
+            } else {
+                // layer-1 mix: per column a broadcast LDS.128 (w0,w1,w2,b), 3 FFMA, tanh, FFMA, pack
+                const float4 w0 = sw[(n * NI + i) & 255], w1 = sw[(n * NI + i + 1) & 255];
+                const float a0 = fmaf(w0.x, x0, fmaf(w0.y, x1, fmaf(w0.z, b, w0.w)));
+                const float a1 = fmaf(w1.x, x0, fmaf(w1.y, x1, fmaf(w1.z, b, w1.w)));
+                acc ^= pack(fmaf(a0, tanh_a(a0), a0), fmaf(a1, tanh_a(a1), a1));
             }
         }
     }
@@ -74,10 +82,10 @@ int main() {
     cudaMalloc(&out, 1 << 24);
     cudaMalloc(&cyc, 1 << 16);
     const char* names[] = {"pack only (+fadd)", "silu fp32 no pack", "silu + pack", "relu + pack", "silu+pack+dot",
-                           "silu + prmt-trunc"};
-    void (*fs[])(uint32_t*, long long*, float) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>};
+                           "silu + prmt-trunc", "layer1 (lds+3ffma+silu+pack)"};
+    void (*fs[])(uint32_t*, long long*, float) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>};
     for (int threads : {256, 512}) {
-        for (int m = 0; m < 6; ++m) {
+        for (int m = 0; m < 7; ++m) {
             fs[m]<<<148, threads>>>(out, cyc, 0.01f);
             fs[m]<<<148, threads>>>(out, cyc, 0.01f);
             cudaDeviceSynchronize();

@@ -32,6 +32,16 @@ __global__ void k(float* out, long long* cyc) {
                 y = __uint_as_float(r);
             }
             if constexpr (OP == 5) asm volatile("fma.rn.f32 %0, %1, %1, %1;" : "=f"(y) : "f"(v[i]));
+            if constexpr (OP == 6) {
+                uint32_t x = __float_as_uint(v[i]), r;
+                asm volatile("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+                y = __uint_as_float(r);
+            }
+            if constexpr (OP == 7) {
+                uint32_t x = __float_as_uint(v[i]), r;
+                asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+                y = __uint_as_float(r);
+            }
             v[i] = y * 0.5f;
         }
     }
@@ -47,11 +57,11 @@ int main() {
     long long* cyc;
     cudaMalloc(&out, 1 << 24);
     cudaMalloc(&cyc, 1 << 16);
-    const char* names[] = {"tanh.f32", "ex2.f32", "rcp.f32", "tanh.bf16x2", "ex2.bf16x2", "fma(+fmul)"};
+    const char* names[] = {"tanh.f32", "ex2.f32", "rcp.f32", "tanh.bf16x2", "ex2.bf16x2", "fma(+fmul)", "tanh.f16x2", "ex2.f16x2"};
     for (int threads : {256, 512, 1024}) {
-        for (int op = 0; op < 6; ++op) {
+        for (int op = 0; op < 8; ++op) {
             auto launch = [&](void (*f)(float*, long long*)) { f<<<148, threads>>>(out, cyc); };
-            void (*f)(float*, long long*) = op == 0 ? k<0> : op == 1 ? k<1> : op == 2 ? k<2> : op == 3 ? k<3> : op == 4 ? k<4> : k<5>;
+            void (*f)(float*, long long*) = op == 0 ? k<0> : op == 1 ? k<1> : op == 2 ? k<2> : op == 3 ? k<3> : op == 4 ? k<4> : op == 5 ? k<5> : op == 6 ? k<6> : k<7>;
             launch(f);
             cudaDeviceSynchronize();
             launch(f);

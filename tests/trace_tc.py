@@ -14,8 +14,8 @@ import synth  # noqa: E402
 from tests import gpu_helpers as gh  # noqa: E402
 
 EV = {0: "mma.wait", 1: "mma.issue", 2: "mma.done_issue", 3: "epi.wait", 4: "epi.got", 5: "epi.unit_done",
-      6: "L1.start", 7: "L1.end", 8: "tile.out", 9: "epi.ld_done", 10: "epi.dfree_sent", 11: "epi.computed",
-      12: "epi.st_done"}
+      6: "L1.start", 7: "L1.end", 8: "tile.out", 9: "epi.ld_done", 10: "epi.dfree_sent", 11: "L1.rows_ready",
+      12: "L1.computed"}
 
 
 def main():
