@@ -37,7 +37,26 @@ __device__ __forceinline__ float act_f32(int a, float x) {
 
 __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
 
+// Standard normals of (global sample g, step t, iteration step): Philox4x32-10 (key = seed, counter =
+// (g, t, step_lo, step_hi)), u = ((x >> 9) + 0.5) 2^-23, Box-Muller on (u0,u1), (u2,u3) (reading R24').
+__device__ __forceinline__ float4 philox_normals(unsigned long long g, int t, unsigned long long step,
+                                                 unsigned long long seed) {
+    uint32_t c[4] = {(uint32_t)g, (uint32_t)t, (uint32_t)step, (uint32_t)(step >> 32)};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const float s23 = 1.1920928955078125e-07f;  // 2^-23
+    const float u0 = ((float)(c[0] >> 9) + 0.5f) * s23, u1 = ((float)(c[1] >> 9) + 0.5f) * s23;
+    const float u2 = ((float)(c[2] >> 9) + 0.5f) * s23, u3 = ((float)(c[3] >> 9) + 0.5f) * s23;
+    // fast SFU forms (MUFU.LG2 / SIN / COS, abs error ~2^-21 on these ranges):
+    // cos(2 pi u) = -cos(theta), sin(2 pi u) = -sin(theta), theta = 2 pi (u - 1/2) in [-pi, pi)
+    const float r0 = sqrtf(-2.f * __logf(u0)), r1 = sqrtf(-2.f * __logf(u2));
+    float s0, c0, s1, c1;
+    __sincosf(6.283185307179586f * (u1 - 0.5f), &s0, &c0);
+    __sincosf(6.283185307179586f * (u3 - 0.5f), &s1, &c1);
+    return make_float4(-r0 * c0, -r0 * s0, -r1 * c1, -r1 * s1);
+}
+
 // ------------------------------------------------------------------ K0: noise + warm-start shift
+// (debug / standalone form; the step graph fuses both into k_rollout)
 // Thread i < n_ctrl*T: U_nom[b][t] = U_out[b][min(t + (step>0), T-1)] (PAPER.md:144 shift).
 // Thread i < T*n_ctrl*K (gen): Philox4x32-10(key = seed, ctr = (g, t, step_lo, step_hi)), g = global
 // sample index b*K_global + k_offset + k; u = ((x >> 9) + 0.5) 2^-23; Box-Muller -> 4 normals.
@@ -55,18 +74,7 @@ __global__ void __launch_bounds__(256) k_noise_shift(Params p, Buffers b, int ge
         const long long j = i - (long long)t * NK;
         const int bb = (int)(j / p.K), k = (int)(j - (long long)bb * p.K);
         const unsigned long long g = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
-        uint32_t c[4] = {(uint32_t)g, (uint32_t)t, (uint32_t)step, (uint32_t)(step >> 32)};
-        philox4x32_10(c, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-        const float s23 = 1.1920928955078125e-07f;  // 2^-23
-        const float u0 = ((float)(c[0] >> 9) + 0.5f) * s23, u1 = ((float)(c[1] >> 9) + 0.5f) * s23;
-        const float u2 = ((float)(c[2] >> 9) + 0.5f) * s23, u3 = ((float)(c[3] >> 9) + 0.5f) * s23;
-        // fast SFU forms (MUFU.LG2 / SIN / COS, abs error ~2^-21 on these ranges):
-        // cos(2 pi u) = -cos(theta), sin(2 pi u) = -sin(theta), theta = 2 pi (u - 1/2) in [-pi, pi)
-        const float r0 = sqrtf(-2.f * __logf(u0)), r1 = sqrtf(-2.f * __logf(u2));
-        float s0, c0, s1, c1;
-        __sincosf(6.283185307179586f * (u1 - 0.5f), &s0, &c0);
-        __sincosf(6.283185307179586f * (u3 - 0.5f), &s1, &c1);
-        b.noise[i] = make_float4(-r0 * c0, -r0 * s0, -r1 * c1, -r1 * s1);
+        b.noise[i] = philox_normals(g, t, step, p.seed);
     }
 }
 
@@ -93,9 +101,19 @@ __device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, fl
 
 constexpr int kRolloutBlock = 64;   // small blocks: K/64 blocks spread the latency-bound rollout over all SMs
 
+// DEV: generate the noise in registers (Philox, one step ahead) and store it for k_softmin; otherwise
+// read the externally set noise. The warm-start shift is fused: the nominal is read from U_out at the
+// shifted index, and block 0 of each controller writes the shifted copy U_nom for k_softmin.
+template <bool DEV>
 __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) {
     const int bb = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long step = *b.step;
+    const int sh = step > 0 ? 1 : 0;
+    if (blockIdx.x == 0)
+        for (int t = threadIdx.x; t < p.T; t += blockDim.x)
+            reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] =
+                reinterpret_cast<const float4*>(b.U_out)[(long long)bb * p.T + min(t + sh, p.T - 1)];
     if (k >= p.K) return;
     const float* x0 = b.x0 + bb * 10;
     float x[10];
@@ -107,20 +125,22 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
     for (int i = 0; i < 9; ++i) R[i] = __ldg(Tq + i);
 #pragma unroll
     for (int i = 0; i < 3; ++i) { tq[i] = __ldg(Tq + 9 + i); gc[i] = __ldg(b.goal + bb * 3 + i); }
-    const float4* Un = reinterpret_cast<const float4*>(b.U_nom) + (long long)bb * p.T;
+    const float4* Uo = reinterpret_cast<const float4*>(b.U_out) + (long long)bb * p.T;
     const long long NK = (long long)p.n_ctrl * p.K;
     const long long col = (long long)bb * p.K + k;
+    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity;
     float part = 0.f;
-    // software pipelining: the noise / nominal of step t+1 are loaded while step t integrates
-    float4 n_next = b.noise[col];
-    float4 U_next = Un[0];
+    // software pipelining: the noise / nominal of step t+1 are produced while step t integrates
+    float4 n_next = DEV ? philox_normals(gidx, 0, step, p.seed) : b.noise[col];
+    float4 U_next = Uo[min(sh, p.T - 1)];
     for (int t = 0; t < p.T; ++t) {
         const float4 n = n_next;
         const float4 U = U_next;
+        if (DEV) b.noise[(long long)t * NK + col] = n;   // for k_softmin (and the debug copy)
         if (t + 1 < p.T) {
-            n_next = b.noise[(long long)(t + 1) * NK + col];
-            U_next = Un[t + 1];
+            n_next = DEV ? philox_normals(gidx, t + 1, step, p.seed) : b.noise[(long long)(t + 1) * NK + col];
+            U_next = Uo[min(t + 1 + sh, p.T - 1)];
         }
         const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
         const float u1 = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
@@ -165,9 +185,10 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
     b.partial[col] = part;
 }
 
-void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s) {
+void launch_rollout(const Params& p, const Buffers& b, bool device_noise, cudaStream_t s) {
     dim3 grid((p.K + kRolloutBlock - 1) / kRolloutBlock, p.n_ctrl);
-    k_rollout<<<grid, kRolloutBlock, 0, s>>>(p, b);
+    if (device_noise) k_rollout<true><<<grid, kRolloutBlock, 0, s>>>(p, b);
+    else k_rollout<false><<<grid, kRolloutBlock, 0, s>>>(p, b);
 }
 
 // ------------------------------------------------------------------ K2f: fp32 SDF-MLP on CUDA cores
@@ -286,7 +307,8 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     if (k < p.K) {
         float acc = b.partial[(long long)bb * p.K + k];
         const float* tp = b.terms + (long long)bb * p.T * p.K + k;
-        for (int t = 0; t < p.T; ++t) acc += tp[(long long)t * p.K];
+#pragma unroll 10
+        for (int t = 0; t < p.T; ++t) acc += __ldcs(tp + (long long)t * p.K);   // streamed once
         J = isfinite(acc) ? acc : INFINITY;
         b.J[(long long)bb * p.K + k] = J;
     }

@@ -434,9 +434,8 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
         if (prof) cudaEventRecordWithFlags(ctx->prof_ev[i], s, cudaEventRecordExternal);
     };
     mark(0);
-    launch_noise_shift(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
-    mark(1);
-    launch_rollout(p, ctx->b, s);
+    mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
+    launch_rollout(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
     mark(2);
     cudaError_t e = launch_mlp_states(ctx, s);
     if (e != cudaSuccess) return e;
@@ -629,8 +628,8 @@ int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
 
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
     if (!ctx) return 0;
-    // noise+shift, rollout, mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL)
-    return 4 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
+    // rollout (+ noise + shift), mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL)
+    return 3 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
 }
 
 }  // extern "C"

@@ -56,7 +56,7 @@ struct Buffers {
 
 // Launchers (kernels_simt.cu)
 void launch_noise_shift(const Params& p, const Buffers& b, bool gen_noise, cudaStream_t s);
-void launch_rollout(const Params& p, const Buffers& b, cudaStream_t s);
+void launch_rollout(const Params& p, const Buffers& b, bool device_noise, cudaStream_t s);   // + noise + shift
 void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s);
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s);
