@@ -149,11 +149,12 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
  * (device fp32) to d_out. Asynchronous on cfg.stream. */
 mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int64_t n, float* d_out);
 
-/* Profiling: when on, every step records CUDA events between its kernels (on cfg.stream);
+/* Profiling: level 1 records CUDA events (captured in the step graph) around the SDF-MLP launch only;
+ * level 2 around every stage (each event node costs ~2 us of step time); 0 off.
  * mppi_get_kernel_times() synchronises and returns the last step's per-stage device times in ms:
- * out[0] noise+shift, [1] rollout, [2] SDF-MLP, [3] softmin (cost + min + weights + update or record),
- * [4] NCCL exchange + combine (0 unless sharded with NCCL). n_out <= 5. */
-mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t on);
+ * out[0] (noise + shift, fused into the rollout: ~0), [1] rollout, [2] SDF-MLP, [3] softmin (cost + min +
+ * weights + update or record), [4] NCCL exchange + combine; stages not measured at level 1 read 0. */
+mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t level);
 mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out);
 /* Number of kernels this library launches per mppi_step (for the bench's gpu_launches count). */
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx);

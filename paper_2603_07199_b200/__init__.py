@@ -159,8 +159,10 @@ class Controller:
                                            C.c_void_p(out.data_ptr())))
         return out
 
-    def set_profiling(self, on: bool):
-        _lib._check(self.lib.mppi_set_profiling(self.ctx, 1 if on else 0))
+    def set_profiling(self, level):
+        """0 off, 1 events around the SDF-MLP launch, 2 every stage (True -> 2)."""
+        level = 2 if level is True else int(level)
+        _lib._check(self.lib.mppi_set_profiling(self.ctx, level))
 
     def kernel_times(self) -> np.ndarray:
         out = np.zeros(5, np.float32)

@@ -119,7 +119,7 @@ struct mppi_ctx {
     int stage_i = 0;
     // graphs: [0] full step, [1] local (record) step
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    bool profiling = false;
+    int profiling = 0;   // 0 off, 1 events around the SDF-MLP launch only, 2 every stage boundary
     cudaEvent_t prof_ev[kNumStages + 1] = {};
     bool prof_valid = false;
     ncclComm_t comm = nullptr;
@@ -429,9 +429,10 @@ static cudaError_t launch_mlp_states(mppi_ctx* ctx, cudaStream_t s) {
 // (and NCCL exchange + combine when a communicator exists); mode 1: local step writing the record.
 static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     const Params& p = ctx->p;
-    const bool prof = ctx->profiling;
+    const int prof = ctx->profiling;
     auto mark = [&](int i) {
-        if (prof) cudaEventRecordWithFlags(ctx->prof_ev[i], s, cudaEventRecordExternal);
+        if (prof >= 2 || (prof == 1 && (i == 2 || i == 3)))
+            cudaEventRecordWithFlags(ctx->prof_ev[i], s, cudaEventRecordExternal);
     };
     mark(0);
     mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
@@ -511,7 +512,7 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph[mode], s));
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_out, s));
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
-    ctx->prof_valid = ctx->profiling;
+    ctx->prof_valid = ctx->profiling > 0;
     ctx->last_mode = mode;
     return MPPI_OK;
 }
@@ -603,10 +604,11 @@ mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int6
     return MPPI_OK;
 }
 
-mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t on) {
+mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t level) {
     CHECK_CTX(ctx);
-    if ((bool)on != ctx->profiling) {
-        ctx->profiling = on != 0;
+    if (level < 0 || level > 2) return fail(MPPI_ERR_INVALID, "profiling level must be 0, 1 or 2");
+    if (level != ctx->profiling) {
+        ctx->profiling = level;
         invalidate_graphs(ctx);
     }
     return MPPI_OK;
@@ -617,7 +619,10 @@ mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out) {
     if (!out || n_out < 1 || n_out > kNumStages) return fail(MPPI_ERR_INVALID, "bad out");
     if (!ctx->prof_valid) return fail(MPPI_ERR_NOT_READY, "no profiled step yet");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < n_out; ++i) CUDA_TRY(ctx, cudaEventElapsedTime(out + i, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+    for (int i = 0; i < n_out; ++i) {
+        out[i] = 0.f;
+        if (ctx->profiling >= 2 || i == 2) CUDA_TRY(ctx, cudaEventElapsedTime(out + i, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+    }
     return MPPI_OK;
 }
 

@@ -33,7 +33,7 @@ def stats(name, **over):
 def timing(name, steps=20):
     import torch
     cfg, Ws, bs, inp, ctrl = gh.setup(name, noise_mode="device")
-    ctrl.set_profiling(True)
+    ctrl.set_profiling(2)
     for i in range(3):
         ctrl.step(inp["x0"], inp["goal"], i)
     ctrl.get_controls()
