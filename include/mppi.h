@@ -72,7 +72,8 @@ typedef struct {
     int32_t noise_mode;                         /* MPPI_NOISE_*                                     */
     uint64_t seed;                              /* Philox key (device noise)                        */
     int32_t world_size, rank;                   /* sample sharding over ranks (configs[3])          */
-    const void* nccl_unique_id;                 /* 128-byte ncclUniqueId; NULL: no NCCL (split-phase) */
+    const void* nccl_unique_id;                 /* 128-byte ncclUniqueId; NULL: no NCCL (split-phase).
+                                                   Non-NULL also with world_size 1 (exercises the path) */
     int32_t device;                             /* CUDA device ordinal                              */
     void* stream;                               /* cudaStream_t all work is enqueued on (0: legacy) */
 } mppi_config;

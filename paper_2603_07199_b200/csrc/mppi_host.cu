@@ -285,7 +285,9 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         cudaMemsetAsync(b.flags, 0, 4 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess)
         return cleanup(MPPI_ERR_CUDA, "memset");
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "sync");
-    if (cfg->world_size > 1 && cfg->nccl_unique_id) {
+    // A communicator is created whenever an id is given (also for world_size 1: the record ->
+    // ncclAllGather -> combine path then runs inside the step graph on a single GPU)
+    if (cfg->nccl_unique_id) {
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world_size, id, cfg->rank);
@@ -441,8 +443,7 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     cudaError_t e = launch_mlp_states(ctx, s);
     if (e != cudaSuccess) return e;
     mark(3);
-    const bool sharded = ctx->cfg.world_size > 1;
-    if (mode == 1 || (sharded && ctx->comm)) {
+    if (mode == 1 || ctx->comm) {
         launch_softmin(p, ctx->b, true, s);
         mark(4);
         if (mode == 0) {
@@ -634,7 +635,7 @@ int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
     if (!ctx) return 0;
     // rollout (+ noise + shift), mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL)
-    return 3 + ((ctx->cfg.world_size > 1 && ctx->comm) ? 1 : 0);
+    return 3 + (ctx->comm ? 1 : 0);
 }
 
 }  // extern "C"

@@ -354,3 +354,25 @@ def test_full_size_sampled_parity(name):
         prop = gh.softmin_property(cfg, U[b], noise[:, b * cfg.K:(b + 1) * cfg.K], J[b])
         assert np.abs(Ug[b] - prop).max() <= gh.ABS_U
     ctrl.close()
+
+
+def test_nccl_exchange_path_single_rank():
+    """The sharded step's NCCL path (record -> ncclAllGather captured in the step graph -> combine)
+    with a world_size-1 communicator must equal the unsharded update (same noise, same costs)."""
+    from paper_2603_07199_b200 import Controller, nccl_unique_id
+    cfg = synth.get_config("c3s")
+    Ws, bs = synth.make_weights(cfg)
+    z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
+                          synth.make_goals(cfg), synth.make_nominal(cfg))
+    outs = []
+    for nid in (None, nccl_unique_id()):
+        c = Controller(cfg, noise_mode="device", nccl_id=nid)
+        c.set_sdf_weights(Ws, bs)
+        c.set_latent(z, Tq)
+        c.set_nominal(U)
+        for step in range(3):   # warm-started steps: graph replay incl. the collective
+            c.step(x0, goal, step)
+        outs.append((c.get_controls()[0], c.kernels_per_step()))
+        c.close()
+    assert outs[1][1] == outs[0][1] + 1     # + k_combine
+    np.testing.assert_allclose(outs[1][0], outs[0][0], atol=1e-5)
