@@ -57,13 +57,13 @@ __device__ unsigned long long g_tc_trace[4][3][kTraceCap];
 #define TC_TRACE_DECL
 #endif
 
-#ifndef MPPI_EPI_WARPS
-#define MPPI_EPI_WARPS 16
-#endif
-constexpr int kEpiWarps = MPPI_EPI_WARPS;   // 8 or 16 (2 or 4 per SMSP)
+constexpr int kEpiWarps = 16;   // 4 per SMSP
 constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 weight loader, 2-3 idle
-constexpr int kCW = 16;         // TMEM columns per epilogue load (register budget: 96/thread)
+// setmaxnreg split of the CTA register pool (640 threads launched at 96 registers): warpgroup 0
+// (issuer, loader) 32, the four epilogue warpgroups 112: 128 x 32 + 512 x 112 = 640 x 96
+constexpr int kRegsCtl = 32, kRegsEpi = 112;
+constexpr int kCW = 16;         // TMEM columns per epilogue load
 constexpr int kTileRows = 128;
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -111,7 +111,7 @@ template <bool kCluster = false>
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
     while (!mbar_try_wait<kCluster>(bar, parity)) {
-        if (++n > (1u << 26)) __trap();
+        if (++n > (1u << 22)) __trap();
     }
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -174,6 +174,14 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
                  : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld tied to the registers of the load it completes, so no use of them can be scheduled above it
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -220,23 +228,41 @@ __device__ __forceinline__ float act_pre(float pre) {
     }
 }
 
+// bf16x2 of act(x0) (low half) and act(x1) (high half); ReLU is fused into the conversion
+// (cvt.rn.relu: relu(rne(x)) = rne(relu(x)), the sign survives rounding).
+template <int ACT>
+__device__ __forceinline__ uint32_t act_pack(float x0, float x1) {
+    if constexpr (ACT == MPPI_ACT_RELU) {
+        uint32_t r;
+        asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x1), "f"(x0));
+        return r;
+    } else {
+        return pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+    }
+}
+
 // ------------------------------------------------------------------ configuration
 template <int H, int G>
 struct Cfg {
     static constexpr int CG = H == 256 ? 2 : 1;              // CTAs per MMA (cta_group)
-    static constexpr int HALF = H / 2;                       // N (and K) extent of one MMA unit
-    static constexpr int ROWS_B = HALF / CG;                 // weight rows (N) of a unit held per CTA
-    static constexpr int UNIT_BYTES = ROWS_B * HALF * 2;     // bf16 B block of one unit in one CTA
-    static constexpr int W_BYTES = G * 4 * UNIT_BYTES;       // resident weights per CTA
-    static constexpr int SLOT_COLS = H;                      // per slot: D [0, HALF) fp32, A [HALF, H) bf16x2
-    static constexpr int NSLOT = 512 / SLOT_COLS;            // tiles in flight per CTA: 2 (H=256), 4 (H=128)
+    // A TS-form MMA (A in TMEM) streams 4 KB of A per K=16 step per CTA (M = 128): below N = 128 it runs
+    // at the A-read rate, not the math rate, so units are N = 128 (two per layer for H = 256, one for 128)
+    static constexpr int NH = H / 128;                       // MMA units (N blocks) per GEMM layer
+    static constexpr int UN = H / NH;                        // N of one unit (128)
+    static constexpr int RB = UN / CG;                       // weight rows (N) of a unit held per CTA
+    static constexpr int UNIT_BYTES = RB * H * 2;            // bf16 B block of one unit in one CTA
+    static constexpr int W_BYTES = G * NH * UNIT_BYTES;      // resident weights per CTA
+    static constexpr int A_OFF = UN;                         // per slot: D [0, UN) fp32, A [UN, UN + H/2) bf16x2
+    static constexpr int SLOT_COLS = 256;
+    static constexpr int NSLOT = 512 / SLOT_COLS;            // tiles in flight per CTA: 2
     static constexpr int TMEM_COLS = NSLOT * SLOT_COLS;      // = 512
-    static constexpr int GW = kEpiWarps / NSLOT;             // epilogue warps per slot group (8 or 4)
+    static constexpr int GW = kEpiWarps / NSLOT;             // epilogue warps per slot group (8)
     static constexpr int COLG = GW / 4;                      // column groups per TMEM lane quarter in a group
     static constexpr int NROWBUF = 2 * NSLOT;                // query-row buffers (prefetch one slot-tile ahead)
-    static constexpr int QW = HALF / COLG;                   // epilogue columns per warp per unit
+    static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
+    static_assert(A_OFF + H / 2 <= SLOT_COLS && QW % kCW == 0 && RB % 8 == 0, "TMEM / unit layout");
     // smem carve-up (offsets from the 1024-aligned base)
     static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
     static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
@@ -316,32 +342,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lbar0 = CG == 2 ? map_to_rank(bar0, 0) : bar0;
     auto lbar = [&](int i) { return lbar0 + 8u * (uint32_t)i; };
 
-    if (warp == 1) {
-        // ================= weight loader: this CTA's half of every unit, once
+    if (warp < kEpiWarp0) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+      if (warp == 1) {
+        // ================= weight loader: this CTA's share of every unit, once
         if (lane == 0 && group < n_tiles) {
             mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)C::W_BYTES);
             const uint8_t* src = wimg + (size_t)rank * C::W_BYTES;
-            for (int u = 0; u < G * 4; ++u)
+            for (int u = 0; u < G * C::NH; ++u)
                 bulk_g2s(sbase + (uint32_t)(u * C::UNIT_BYTES), src + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
                          bar(BAR_WLOCAL));
             mbar_wait(bar(BAR_WLOCAL), 0);
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
             else mbar_arrive_local(bar(BAR_WREADY));
         }
-    } else if (warp == 0) {
+      } else if (warp == 0) {
         // ================= MMA issuer (one thread of the leader CTA)
         // NSLOT tiles in flight (TMEM slots). Per layer and N-half h, one full-K unit per slot, issued slot by
         // slot (X(h0) Y(h0) .. X(h1) Y(h1) ..): while the epilogue drains one slot the tensor pipe works on
         // the others.
         if (lane == 0 && leader && group < n_tiles) {
-            constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::HALF);
+            constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::UN);
             const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
             uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
             for (long long i0 = 0; i0 < n_my; i0 += C::NSLOT) {
                 const int ns = (int)min((long long)C::NSLOT, n_my - i0);
                 for (int l = 0; l < G; ++l)
-                    for (int h = 0; h < 2; ++h)
+                    for (int h = 0; h < C::NH; ++h)
                         for (int sl = 0; sl < ns; ++sl) {
                             TC_TRACE(0, 0, l, h, sl, i0);
                             if (h == 0) mbar_wait<CG == 2>(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
@@ -350,12 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tc_fence_after();
                             TC_TRACE(0, 1, l, h, sl, i0);
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
-                            const uint32_t a_t = d_t + (uint32_t)C::HALF;
+                            const uint32_t a_t = d_t + (uint32_t)C::A_OFF;
+                            const uint32_t b_unit = sbase + (uint32_t)((l * C::NH + h) * C::UNIT_BYTES);
 #pragma unroll
                             for (int j = 0; j < H / 16; ++j) {
-                                const int kk = j * 16, c = kk / C::HALF, kin = kk % C::HALF;
-                                const uint32_t b_addr = sbase + (uint32_t)(((l * 2 + h) * 2 + c) * C::UNIT_BYTES) +
-                                                        (uint32_t)((kin / 64) * (C::ROWS_B * 128) + (kin % 64) * 2);
+                                const int kk = j * 16;
+                                const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
                                 tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, j > 0 ? 1u : 0u);
                             }
                             tc_commit<CG>(bar(BAR_MMA + sl));
@@ -363,7 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
             }
         }
-    } else if (warp >= kEpiWarp0) {
+      }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
         // ================= epilogue: NSLOT groups of GW warps, group sl owns TMEM slot sl and the CTA's
         // tiles i = sl, sl + NSLOT, ... (one group computes while the others wait for their MMA units)
         constexpr int kColGroups = C::COLG;
@@ -433,12 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
             const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
-            const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
+            const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < C::NH; ++c) {
 #pragma unroll
                 for (int k = 0; k < C::NCH; ++k) {
-                    const int j0 = c * C::HALF + cgi * C::QW + k * kCW;
+                    const int j0 = c * C::UN + cgi * C::QW + k * kCW;
                     uint32_t packed[kCW / 2];
                     if (!any_far) {
 #pragma unroll
@@ -446,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float4 w0 = w1g[j0 + i2], w1 = w1g[j0 + i2 + 1];
                             const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, w0.w)));
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
-                            packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                            packed[i2 / 2] = act_pack<ACT>(x0, x1);
                         }
                     } else {   // rare: the tile crosses a controller boundary
 #pragma unroll
@@ -456,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : w1.w;
                             const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, b0)));
                             const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, b1)));
-                            packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
+                            packed[i2 / 2] = act_pack<ACT>(x0, x1);
                         }
                     }
                     tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
@@ -473,32 +503,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_rows(sl);
         if (sl < n_my) layer1(sl);
         for (long long i = sl; i < n_my; i += C::NSLOT) {
-            uint32_t keep[C::QW / 2];                 // h0 activations (bf16x2) until h1 is done
+            uint32_t keep[C::NH > 1 ? C::QW / 2 : 1];   // unit-0 activations (bf16x2) until unit 1 is done
             float sdot = 0.f;
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
                 const float* hb = s_hb + l * H;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < C::NH; ++h) {
                     if (tracer) TC_TRACE(trole, 3, l, h, sl, i);
                     mbar_wait(bar(BAR_MMA + sl), (mma_cnt++) & 1);
                     tc_fence_after();
                     if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
                     const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
-                    const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::HALF);
+                    const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
 #pragma unroll
                     for (int k = 0; k < C::NCH; ++k) {
                         uint32_t acc[kCW];
                         tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
-                        tmem_wait_ld();
+                        tmem_wait_ld_regs(acc);
                         if (k == C::NCH - 1) {   // D of the slot may be overwritten now
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) arrive_sched(BAR_DFREE + sl);
                             if (tracer) TC_TRACE(trole, 10, l, h, sl, i);
                         }
-                        const int j0 = h * C::HALF + cgi * C::QW + k * kCW;   // output neuron index
+                        const int j0 = h * C::UN + cgi * C::QW + k * kCW;   // output neuron index
                         if (!last) {
                             uint32_t packed[kCW / 2];
 #pragma unroll
@@ -508,15 +538,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const float x1 = fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y);
                                 const float x2 = fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z);
                                 const float x3 = fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w);
-                                packed[i2 / 2] = pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
-                                packed[i2 / 2 + 1] = pack_bf16x2(act_pre<ACT>(x2), act_pre<ACT>(x3));
+                                packed[i2 / 2] = act_pack<ACT>(x0, x1);
+                                packed[i2 / 2 + 1] = act_pack<ACT>(x2, x3);
                             }
-                            if (h == 0) {
+                            if (h < C::NH - 1) {
 #pragma unroll
                                 for (int i2 = 0; i2 < kCW / 2; ++i2) keep[k * (kCW / 2) + i2] = packed[i2];
                             } else {
-                                // both N-halves of this layer done: A of the slot is dead -> next input
-                                tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::HALF) / 2), &keep[k * (kCW / 2)]);
+                                // every unit of this layer done: A of the slot is dead -> next input
+                                if constexpr (C::NH > 1)
+                                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::UN) / 2), &keep[k * (kCW / 2)]);
                                 tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                             }
                         } else {
@@ -524,10 +555,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
                                 const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
                                 const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i2);
-                                const uint32_t p0 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i2]), kP, bv.x)),
-                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y)));
-                                const uint32_t p1 = pack_bf16x2(act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z)),
-                                                                act_pre<ACT>(fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w)));
+                                const uint32_t p0 = act_pack<ACT>(fmaf(__uint_as_float(acc[i2]), kP, bv.x),
+                                                                  fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y));
+                                const uint32_t p1 = act_pack<ACT>(fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z),
+                                                                  fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w));
                                 sdot = fmaf(__uint_as_float(p0 << 16), wv.x, sdot);
                                 sdot = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot);
                                 sdot = fmaf(__uint_as_float(p1 << 16), wv.z, sdot);
@@ -535,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (!last && h == 1) {
+                    if (!last && h == C::NH - 1) {
                         tmem_wait_st();
                         tc_fence_before();
                         __syncwarp();
@@ -654,32 +685,32 @@ bool mlp_tc_supported(int H, int G, int act) {
 
 size_t mlp_tc_weight_bytes(int H, int G) { return (size_t)G * H * H * 2; }
 
-// Global image = the shared-memory images of the CTA(s) of one MMA group, [rank][layer][N-half h]
-// [K-half c] blocks of ROWS_B x HALF bf16 (rank r holds rows [h HALF + r ROWS_B, +ROWS_B) of W_l);
-// inside a block, [64-wide K chunk][row n][128 B] with the 16-byte groups of row n XOR-swizzled by
-// (n % 8) (UMMA SWIZZLE_128B, K-major, 8-row atoms of 1024 B).
+// Global image = the shared-memory images of the CTA(s) of one MMA group, [rank][layer][unit q] blocks
+// of RB x H bf16 (rank r holds rows [q UN + r RB, +RB) of W_l, UN = H/NH, RB = UN/CG); inside a block,
+// [64-wide K chunk][row n][128 B] with the 16-byte groups of row n XOR-swizzled by (n % 8) (UMMA
+// SWIZZLE_128B, K-major, 8-row atoms of 1024 B).
 void mlp_tc_pack_weights(int H, int G, const float* W, uint8_t* out) {
-    const int HALF = H / 2, CG = H == 256 ? 2 : 1, RB = HALF / CG;
-    const size_t unit = (size_t)RB * HALF * 2;
-    const size_t per_rank = (size_t)G * 4 * unit;
+    const int CG = H == 256 ? 2 : 1, NU = H == 256 ? tc::Cfg<256, 1>::NH : tc::Cfg<128, 1>::NH;
+    const int UN = H / NU, RB = UN / CG;
+    const size_t unit = (size_t)RB * H * 2;
+    const size_t per_rank = (size_t)G * NU * unit;
     for (int r = 0; r < CG; ++r)
         for (int l = 0; l < G; ++l)
-            for (int h = 0; h < 2; ++h)
-                for (int c = 0; c < 2; ++c) {
-                    uint8_t* blk = out + (size_t)r * per_rank + (size_t)((l * 2 + h) * 2 + c) * unit;
-                    for (int nn = 0; nn < RB; ++nn)
-                        for (int kk = 0; kk < HALF; ++kk) {
-                            const int n = h * HALF + r * RB + nn, k = c * HALF + kk;
-                            const float v = W[(size_t)l * H * H + (size_t)n * H + k];
-                            uint32_t u;
-                            std::memcpy(&u, &v, 4);   // already a bf16 value: the top 16 bits are exact
-                            const uint16_t bits = (uint16_t)(u >> 16);
-                            const int kc = kk / 64, w = kk % 64;
-                            const size_t off = (size_t)kc * RB * 128 + (size_t)nn * 128 +
-                                               (size_t)(((w / 8) ^ (nn % 8)) * 16) + (size_t)(w % 8) * 2;
-                            std::memcpy(blk + off, &bits, 2);
-                        }
-                }
+            for (int q = 0; q < NU; ++q) {
+                uint8_t* blk = out + (size_t)r * per_rank + (size_t)(l * NU + q) * unit;
+                for (int nn = 0; nn < RB; ++nn)
+                    for (int k = 0; k < H; ++k) {
+                        const int n = q * UN + r * RB + nn;
+                        const float v = W[(size_t)l * H * H + (size_t)n * H + k];
+                        uint32_t u;
+                        std::memcpy(&u, &v, 4);   // already a bf16 value: the top 16 bits are exact
+                        const uint16_t bits = (uint16_t)(u >> 16);
+                        const int kc = k / 64, w = k % 64;
+                        const size_t off = (size_t)kc * RB * 128 + (size_t)nn * 128 +
+                                           (size_t)(((w / 8) ^ (nn % 8)) * 16) + (size_t)(w % 8) * 2;
+                        std::memcpy(blk + off, &bits, 2);
+                    }
+            }
 }
 
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
@@ -687,8 +718,12 @@ cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows,
 #define MPPI_TC_CASE(HH, GG, AA) \
     if (p.H == HH && p.n_gemm == GG && p.act == AA) return tc::launch_t<HH, GG, AA>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
 #define MPPI_TC_ACTS(HH, GG) MPPI_TC_CASE(HH, GG, 0) MPPI_TC_CASE(HH, GG, 1) MPPI_TC_CASE(HH, GG, 2)
+#ifdef MPPI_TC_QUICK   // development builds: the configs[1..4] instantiations only
+    MPPI_TC_CASE(128, 2, 1) MPPI_TC_CASE(256, 3, 2)
+#else
     MPPI_TC_ACTS(128, 1) MPPI_TC_ACTS(128, 2) MPPI_TC_ACTS(128, 3)
     MPPI_TC_ACTS(256, 1) MPPI_TC_ACTS(256, 2) MPPI_TC_ACTS(256, 3)
+#endif
 #undef MPPI_TC_ACTS
 #undef MPPI_TC_CASE
     return cudaErrorInvalidValue;

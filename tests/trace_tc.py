@@ -56,7 +56,7 @@ def main():
         print(f"--- block {blk}: {len(ev)} events, span {ev[-1][0] - base} cycles")
         for k, role, ci in ev:
             print(f"{k - base:8d} {['MMA', 'EPI0', 'EPI7'][role]:5s} {EV.get((ci >> 8) & 15, '?'):16s} "
-                  f"l={(ci >> 6) & 3} h={(ci >> 5) & 1} c={(ci >> 4) & 1} t={ci & 15}")
+                  f"l={(ci >> 6) & 3} q={(ci >> 4) & 3} t={ci & 15}")
 
 
 if __name__ == "__main__":
