@@ -104,16 +104,21 @@ constexpr int kRolloutBlock = 64;   // small blocks: K/64 blocks spread the late
 // DEV: generate the noise in registers (Philox, one step ahead) and store it for k_softmin; otherwise
 // read the externally set noise. The warm-start shift is fused: the nominal is read from U_out at the
 // shifted index, and block 0 of each controller writes the shifted copy U_nom for k_softmin.
+constexpr int kMaxTStaged = 128;   // nominal staged in shared memory up to this horizon
+
 template <bool DEV>
 __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) {
+    __shared__ float4 s_U[kMaxTStaged];   // the shifted nominal U*_t of this controller (L1-latency reads)
     const int bb = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long step = *b.step;
     const int sh = step > 0 ? 1 : 0;
-    if (blockIdx.x == 0)
-        for (int t = threadIdx.x; t < p.T; t += blockDim.x)
-            reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] =
-                reinterpret_cast<const float4*>(b.U_out)[(long long)bb * p.T + min(t + sh, p.T - 1)];
+    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+        const float4 u = reinterpret_cast<const float4*>(b.U_out)[(long long)bb * p.T + min(t + sh, p.T - 1)];
+        if (t < kMaxTStaged) s_U[t] = u;
+        if (blockIdx.x == 0) reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] = u;
+    }
+    __syncthreads();
     if (k >= p.K) return;
     const float* x0 = b.x0 + bb * 10;
     float x[10];
@@ -129,24 +134,25 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
     const long long NK = (long long)p.n_ctrl * p.K;
     const long long col = (long long)bb * p.K + k;
     const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
-    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity;
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity, inv_mass = 1.f / p.mass;
     float part = 0.f;
     // software pipelining: the noise / nominal of step t+1 are produced while step t integrates
     float4 n_next = DEV ? philox_normals(gidx, 0, step, p.seed) : b.noise[col];
-    float4 U_next = Uo[min(sh, p.T - 1)];
+    auto nominal = [&](int t) { return t < kMaxTStaged ? s_U[t] : Uo[min(t + sh, p.T - 1)]; };
+    float4 U_next = nominal(0);
     for (int t = 0; t < p.T; ++t) {
         const float4 n = n_next;
         const float4 U = U_next;
         if (DEV) b.noise[(long long)t * NK + col] = n;   // for k_softmin (and the debug copy)
         if (t + 1 < p.T) {
             n_next = DEV ? philox_normals(gidx, t + 1, step, p.seed) : b.noise[(long long)(t + 1) * NK + col];
-            U_next = Uo[min(t + 1 + sh, p.T - 1)];
+            U_next = nominal(t + 1);
         }
         const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
         const float u1 = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
         const float u2 = clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]);
         const float u3 = clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]);
-        const float com = u0 / p.mass;
+        const float com = u0 * inv_mass;
         float k1[10], k2[10], k3[10], k4[10], xt[10];
         dyn_ctbr(x, com, u1, u2, u3, g, k1);
 #pragma unroll
@@ -160,9 +166,9 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
         dyn_ctbr(xt, com, u1, u2, u3, g, k4);
 #pragma unroll
         for (int i = 0; i < 10; ++i) x[i] = x[i] + dt6 * (k1[i] + 2.f * k2[i] + 2.f * k3[i] + k4[i]);
-        const float qn = sqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);
+        const float qinv = rsqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);   // MUFU, ~2 ulp
 #pragma unroll
-        for (int i = 6; i < 10; ++i) x[i] = x[i] / qn;
+        for (int i = 6; i < 10; ++i) x[i] = x[i] * qinv;
         // query-frame position and direction, scored at x_{t+1} (reading R7)
         float pc[3], dv[3];
 #pragma unroll
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
         const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
         const long long s = ((long long)bb * p.T + t) * p.K + k;
         if (p.rps == 2) {
-            const float sc = nv >= 1e-6f ? p.fd_h / nv : 0.f;
+            const float sc = nv >= 1e-6f ? __fdividef(p.fd_h, nv) : 0.f;
             b.rows[2 * s] = make_float4(pc[0], pc[1], pc[2], nv);
             b.rows[2 * s + 1] = make_float4(pc[0] + sc * dv[0], pc[1] + sc * dv[1], pc[2] + sc * dv[2], 0.f);
         } else {
@@ -307,8 +313,16 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     if (k < p.K) {
         float acc = b.partial[(long long)bb * p.K + k];
         const float* tp = b.terms + (long long)bb * p.T * p.K + k;
-#pragma unroll 10
-        for (int t = 0; t < p.T; ++t) acc += __ldcs(tp + (long long)t * p.K);   // streamed once
+        // streamed once; 16 independent loads in flight per thread, summed in t order
+        int t = 0;
+        for (; t + 16 <= p.T; t += 16) {
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __ldcs(tp + (long long)(t + i) * p.K);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc += v[i];
+        }
+        for (; t < p.T; ++t) acc += __ldcs(tp + (long long)t * p.K);
         J = isfinite(acc) ? acc : INFINITY;
         b.J[(long long)bb * p.K + k] = J;
     }
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
         if (m < INFINITY) {
-#pragma unroll 4
+#pragma unroll 8
             for (int i = lane; i < kn; i += 32) {
                 const float wi = s_w[i];
                 const float4 n = nz[i];
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     for (int tc = threadIdx.x; tc < 4 * p.T; tc += blockDim.x) {
         float V = 0.f;
         if (ok) {
-#pragma unroll 8
+#pragma unroll 16
             for (int i = 0; i < nblk; ++i) {
                 const float f = i < kSoftminBlock ? s_f[i]
                                                   : expf((mg - __ldcg(recs + (long long)i * W)) * p.inv_lambda);
