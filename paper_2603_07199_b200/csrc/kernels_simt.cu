@@ -284,7 +284,8 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 // records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
 // U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
-constexpr int kSoftminBlock = 256;
+constexpr int kSoftminBlock = 256;     // samples per block
+constexpr int kSoftminThreads = 512;   // two threads per sample in phase 1, 16 warps over t in phase 2
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
     #pragma unroll
@@ -301,34 +302,44 @@ __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) 
     return r;
 }
 
-__global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, int write_record) {
+__global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b, int write_record) {
     __shared__ float s_w[kSoftminBlock];
-    __shared__ float red[kSoftminBlock / 32];
+    __shared__ float s_half[kSoftminBlock];
+    __shared__ float red[kSoftminThreads / 32];
     __shared__ bool s_last;
     const int bb = blockIdx.y, nblk = gridDim.x;
-    const int k = blockIdx.x * kSoftminBlock + threadIdx.x;
+    const int kk = threadIdx.x % kSoftminBlock, half = threadIdx.x / kSoftminBlock;
+    const int k = blockIdx.x * kSoftminBlock + kk;
     const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
-    // ---- phase 1: thread per sample
+    // ---- phase 1: two threads per sample, each summing half of the horizon's terms in t order
     float J = INFINITY;
-    if (k < p.K) {
-        float acc = b.partial[(long long)bb * p.K + k];
-        const float* tp = b.terms + (long long)bb * p.T * p.K + k;
-        // streamed once; 16 independent loads in flight per thread, summed in t order
-        int t = 0;
-        for (; t + 16 <= p.T; t += 16) {
-            float v[16];
+    {
+        const int th = (p.T + 1) / 2, t0 = half * th, t1 = min(p.T, t0 + th);
+        float acc = 0.f;
+        if (k < p.K) {
+            const float* tp = b.terms + (long long)bb * p.T * p.K + k;
+            // streamed once; 16 independent loads in flight per thread
+            int t = t0;
+            for (; t + 16 <= t1; t += 16) {
+                float v[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = __ldcs(tp + (long long)(t + i) * p.K);
+                for (int i = 0; i < 16; ++i) v[i] = __ldcs(tp + (long long)(t + i) * p.K);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc += v[i];
+                for (int i = 0; i < 16; ++i) acc += v[i];
+            }
+            for (; t < t1; ++t) acc += __ldcs(tp + (long long)t * p.K);
         }
-        for (; t < p.T; ++t) acc += __ldcs(tp + (long long)t * p.K);
-        J = isfinite(acc) ? acc : INFINITY;
-        b.J[(long long)bb * p.K + k] = J;
+        if (half == 1) s_half[kk] = acc;
+        __syncthreads();
+        if (half == 0 && k < p.K) {
+            acc = b.partial[(long long)bb * p.K + k] + acc + s_half[kk];
+            J = isfinite(acc) ? acc : INFINITY;
+            b.J[(long long)bb * p.K + k] = J;
+        }
     }
     const float m = block_reduce(J, red, true);
-    const float w = (J < INFINITY) ? expf((m - J) * p.inv_lambda) : 0.f;
-    s_w[threadIdx.x] = w;
+    const float w = (J < INFINITY) ? expf((m - J) * p.inv_lambda) : 0.f;   // 0 for the second half
+    if (half == 0) s_w[kk] = w;
     const float S = block_reduce(w, red, false);
     const float S2 = block_reduce(w * w, red, false);
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
     if (!s_last) return;
     __threadfence();
     const float* recs = b.blkrec + (long long)bb * nblk * W;
-    __shared__ float s_f[kSoftminBlock];   // per-record scale exp((m - m_b)/lambda), nblk <= blocks handled below
+    __shared__ float s_f[kSoftminThreads];   // per-record scale exp((m - m_b)/lambda), nblk <= blocks handled below
     // global min over block records (thread i reads record i; tree with fixed shape)
     float mi_loc = INFINITY;
     for (int i = threadIdx.x; i < nblk; i += blockDim.x) mi_loc = fminf(mi_loc, __ldcg(recs + (long long)i * W));
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
         const float* r = recs + (long long)i * W;
         const float mi = __ldcg(r);
         const float f = (ok && mi < INFINITY) ? expf((mg - mi) * p.inv_lambda) : 0.f;
-        if (i < kSoftminBlock) s_f[i] = f;
+        if (i < kSoftminThreads) s_f[i] = f;
         sl += __ldcg(r + 1) * f;
         s2l += __ldcg(r + 2) * f * f;
     }
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
         if (ok) {
 #pragma unroll 16
             for (int i = 0; i < nblk; ++i) {
-                const float f = i < kSoftminBlock ? s_f[i]
+                const float f = i < kSoftminThreads ? s_f[i]
                                                   : expf((mg - __ldcg(recs + (long long)i * W)) * p.inv_lambda);
                 V = fmaf(__ldcg(recs + (long long)i * W + 4 + tc), f, V);
             }
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(kSoftminBlock) k_softmin(Params p, Buffers b, 
 
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
     dim3 grid((p.K + kSoftminBlock - 1) / kSoftminBlock, p.n_ctrl);
-    k_softmin<<<grid, kSoftminBlock, 0, s>>>(p, b, write_record ? 1 : 0);
+    k_softmin<<<grid, kSoftminThreads, 0, s>>>(p, b, write_record ? 1 : 0);
 }
 
 int softmin_blocks(int K) { return (K + kSoftminBlock - 1) / kSoftminBlock; }
