@@ -145,6 +145,11 @@ enum { MPPI_DBG_QUERIES = 0, MPPI_DBG_SDF = 1, MPPI_DBG_COSTS = 2, MPPI_DBG_NOIS
        MPPI_DBG_PARTIAL = 5, MPPI_DBG_RECORD = 6 };
 mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes);
 
+/* Test support: on != 0 makes every later step also write s per query row (the buffer behind
+ * MPPI_DBG_SDF, 4 B per row of extra HBM traffic); off by default, when MPPI_DBG_SDF returns
+ * MPPI_ERR_NOT_READY. Takes effect from the next step (the step graph is re-captured). */
+mppi_status mppi_set_debug_outputs(mppi_ctx* ctx, int32_t on);
+
 /* Test support: run the production SDF-MLP kernel of this context on n query-frame rows
  * d_rows [n][4] (x, y, z, unused; device fp32) with controller ctrl's folded latent, writing s [n]
  * (device fp32) to d_out. Asynchronous on cfg.stream. */

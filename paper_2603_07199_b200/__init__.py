@@ -33,7 +33,7 @@ class Controller:
 
     def __init__(self, cfg, *, device: int = 0, stream=None, noise_mode: str = "device", world_size: int = 1,
                  rank: int = 0, K_global: int | None = None, k_offset: int = 0, nccl_id: bytes | None = None,
-                 seed: int | None = None):
+                 seed: int | None = None, debug_outputs: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2603_07199_b200.Controller needs a CUDA device (no CPU fallback)")
@@ -58,6 +58,12 @@ class Controller:
         _lib._check(self.lib.mppi_create(C.byref(self.c), C.c_void_p(self.ws_ptr), nbytes, C.byref(self.ctx)))
         self.n, self.K, self.T = cfg.n_ctrl, cfg.K, cfg.T
         self.rps = 2 if cfg.w_guide != 0 else 1
+        if debug_outputs:
+            self.set_debug_outputs(True)
+
+    def set_debug_outputs(self, on: bool):
+        """Test support: also write s per query row in every step (debug("sdf")); off by default."""
+        _lib._check(self.lib.mppi_set_debug_outputs(self.ctx, 1 if on else 0))
 
     def close(self):
         if getattr(self, "ctx", None) and self.ctx.value:

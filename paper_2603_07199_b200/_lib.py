@@ -22,7 +22,7 @@ EXPORTS = ["mppi_workspace_bytes", "mppi_create", "mppi_destroy", "mppi_get_nccl
            "mppi_set_sdf_weights", "mppi_set_latent", "mppi_set_nominal", "mppi_set_noise", "mppi_step",
            "mppi_step_device", "mppi_step_local", "mppi_record_size", "mppi_get_record_device",
            "mppi_step_finish", "mppi_get_controls", "mppi_get_diagnostics", "mppi_debug_copy", "mppi_sdf_eval",
-           "mppi_set_profiling", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_debug_trace",
+           "mppi_set_profiling", "mppi_set_debug_outputs", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_debug_trace",
            "mppi_last_error"]
 
 
@@ -81,6 +81,7 @@ def load(path: str | None = None):
         "mppi_debug_copy": ([vp, i32, vp, sz], i32),
         "mppi_sdf_eval": ([vp, i32, vp, i64, vp], i32),
         "mppi_set_profiling": ([vp, i32], i32),
+        "mppi_set_debug_outputs": ([vp, i32], i32),
         "mppi_get_kernel_times": ([vp, vp, i32], i32),
         "mppi_kernels_per_step": ([vp], i32),
         "mppi_debug_trace": ([vp, i32], i32),

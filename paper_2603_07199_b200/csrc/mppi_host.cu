@@ -120,6 +120,7 @@ struct mppi_ctx {
     // graphs: [0] full step, [1] local (record) step
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     int profiling = 0;   // 0 off, 1 events around the SDF-MLP launch only, 2 every stage boundary
+    int debug_outputs = 0;   // write s per query row in the step (MPPI_DBG_SDF)
     cudaEvent_t prof_ev[kNumStages + 1] = {};
     bool prof_valid = false;
     ncclComm_t comm = nullptr;
@@ -422,8 +423,9 @@ static cudaError_t launch_mlp_states(mppi_ctx* ctx, cudaStream_t s) {
     const Params& p = ctx->p;
     const long long n_states = (long long)p.n_ctrl * p.T * p.K;
     if (ctx->use_tc)
-        return launch_mlp_tc(p, ctx->b, ctx->b.rows, n_states * p.rps, -1, ctx->b.sdf_rows, true, s);
-    launch_mlp_simt(p, ctx->b, ctx->b.rows, n_states, -1, ctx->b.sdf_rows, true, s);
+        return launch_mlp_tc(p, ctx->b, ctx->b.rows, n_states * p.rps, -1, ctx->debug_outputs ? ctx->b.sdf_rows : nullptr,
+                             true, s);
+    launch_mlp_simt(p, ctx->b, ctx->b.rows, n_states, -1, ctx->debug_outputs ? ctx->b.sdf_rows : nullptr, true, s);
     return cudaGetLastError();
 }
 
@@ -573,7 +575,11 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
     size_t need = 0;
     switch (what) {
         case MPPI_DBG_QUERIES: src = ctx->b.rows; need = 16 * states * p.rps; break;
-        case MPPI_DBG_SDF: src = ctx->b.sdf_rows; need = 4 * states * p.rps; break;
+        case MPPI_DBG_SDF:
+            if (!ctx->debug_outputs) return fail(MPPI_ERR_NOT_READY, "MPPI_DBG_SDF needs mppi_set_debug_outputs(ctx, 1)");
+            src = ctx->b.sdf_rows;
+            need = 4 * states * p.rps;
+            break;
         case MPPI_DBG_COSTS: src = ctx->b.J; need = 4 * (size_t)p.n_ctrl * p.K; break;
         case MPPI_DBG_NOISE: src = ctx->b.noise; need = 16 * states; break;
         case MPPI_DBG_TERMS: src = ctx->b.terms; need = 4 * states; break;
@@ -602,6 +608,15 @@ mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int6
         e = cudaGetLastError();
     }
     CUDA_TRY(ctx, e);
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_debug_outputs(mppi_ctx* ctx, int32_t on) {
+    CHECK_CTX(ctx);
+    if ((on != 0) != (ctx->debug_outputs != 0)) {
+        ctx->debug_outputs = on != 0;
+        invalidate_graphs(ctx);
+    }
     return MPPI_OK;
 }
 

@@ -20,7 +20,7 @@ def setup(name, noise_mode="external", step=0, seed=0, weights=None, **over):
     Ws, bs = weights if weights is not None else synth.make_weights(cfg)
     inp = dict(z=synth.make_latents(cfg), Tq=synth.make_query_transforms(cfg), x0=synth.make_x0(cfg),
                goal=synth.make_goals(cfg), U=synth.make_nominal(cfg))
-    ctrl = Controller(cfg, noise_mode=noise_mode)
+    ctrl = Controller(cfg, noise_mode=noise_mode, debug_outputs=True)
     ctrl.set_sdf_weights(Ws, bs)
     ctrl.set_latent(inp["z"], inp["Tq"])
     ctrl.set_nominal(inp["U"])

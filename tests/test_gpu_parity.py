@@ -241,6 +241,24 @@ def test_graph_replay_is_deterministic():
     np.testing.assert_array_equal(out[0][1], out[1][1])
 
 
+def test_debug_outputs_switch_leaves_the_step_unchanged():
+    """mppi_set_debug_outputs only adds the per-row s buffer: with it off, debug("sdf") is NOT_READY and
+    the step's costs and controls are bitwise those of the same step with it on."""
+    from paper_2603_07199_b200 import MppiError
+    cfg, Ws, bs, inp, ctrl = gh.setup("c2s", noise_mode="device")
+    out = []
+    for on in (True, False):
+        ctrl.set_debug_outputs(on)
+        ctrl.set_nominal(inp["U"])
+        ctrl.step(inp["x0"], inp["goal"], 3)
+        out.append((ctrl.get_controls()[0], ctrl.debug("costs"), ctrl.debug("terms")))
+    with pytest.raises(MppiError) as ei:
+        ctrl.debug("sdf")
+    assert ei.value.status == -4
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_closed_loop_warm_start_c1s():
     """configs[1] protocol (reading R19) at reduced size: 6 warm-started steps with shift, latent
     redrawn every 5 steps, the true state advanced by the oracle's RK4 with u0 (teacher forcing:
@@ -326,7 +344,7 @@ def test_full_size_sampled_parity(name):
     Ws, bs = synth.make_weights(cfg)
     z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
                           synth.make_goals(cfg), synth.make_nominal(cfg))
-    ctrl = Controller(cfg, noise_mode="device")
+    ctrl = Controller(cfg, noise_mode="device", debug_outputs=True)
     ctrl.set_sdf_weights(Ws, bs)
     ctrl.set_latent(z, Tq)
     ctrl.set_nominal(U)
