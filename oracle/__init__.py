@@ -42,6 +42,9 @@ class OracleCfg(C.Structure):
         ("latent_dim", C.c_int32), ("hidden", C.c_int32), ("n_hidden", C.c_int32),
         ("activation", C.c_int32), ("mlp_bf16", C.c_int32),
         ("sdf_mode", C.c_int32), ("gate_c", C.c_double), ("gate_tana", C.c_double),
+        ("model", C.c_int32), ("arm", C.c_double), ("kappa", C.c_double), ("inertia", C.c_double * 3),
+        ("thrust_max", C.c_double), ("rate_max", C.c_double),
+        ("q_gate", C.c_double), ("q_vis", C.c_double), ("q_sdf", C.c_double), ("d_safe", C.c_double),
     ]
 
 
@@ -76,6 +79,8 @@ def lib():
         _lib.oracle_step.argtypes = [P(OracleCfg), P(f), P(f), P(f), P(f), P(f), P(f), P(f), P(d),
                                      P(d), P(d), P(d), P(d), P(d), P(d), P(d), P(d), P(d), P(i32)]
         _lib.oracle_shift.argtypes = [i32, i32, P(f)]
+        _lib.oracle_rotor_deriv.argtypes = [P(OracleCfg), P(d), P(d), P(d)]
+        _lib.oracle_rotor_step.argtypes = [P(OracleCfg), P(d), P(d), P(d)]
     return _lib
 
 
@@ -103,6 +108,12 @@ def make_cfg(cfg, sdf_mode: int = 0, gate_c: float = 0.5, gate_tana: float = 0.3
     oc.latent_dim, oc.hidden, oc.n_hidden = cfg.latent_dim, cfg.hidden, cfg.n_hidden
     oc.activation, oc.mlp_bf16 = cfg.activation, int(cfg.mlp_dtype == 1)
     oc.sdf_mode, oc.gate_c, oc.gate_tana = sdf_mode, gate_c, gate_tana
+    oc.model = getattr(cfg, "model", 0)
+    if oc.model == 1:
+        oc.arm, oc.kappa, oc.thrust_max, oc.rate_max = cfg.arm, cfg.kappa, cfg.thrust_max, cfg.rate_max
+        for i in range(3):
+            oc.inertia[i] = cfg.inertia[i]
+        oc.q_gate, oc.q_vis, oc.q_sdf, oc.d_safe = cfg.q_gate, cfg.q_vis, cfg.q_sdf, cfg.d_safe
     for k, v in override.items():
         setattr(oc, k, v)
     return oc
@@ -139,6 +150,22 @@ def rk4_step(x, u, dt, m, g):
     return out
 
 
+def rotor_deriv(oc: OracleCfg, x, u):
+    """Paper model (model 1): xdot for x [17], u [4]."""
+    x, u = _f64(x), _f64(u)
+    out = np.zeros(17)
+    lib().oracle_rotor_deriv(C.byref(oc), _p(x, C.c_double), _p(u, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def rotor_step(oc: OracleCfg, x, u):
+    """Paper model (model 1): one RK4 step of oc.dt with the post-step renormalisation and clamps."""
+    x, u = _f64(x), _f64(u)
+    out = np.zeros(17)
+    lib().oracle_rotor_step(C.byref(oc), _p(x, C.c_double), _p(u, C.c_double), _p(out, C.c_double))
+    return out
+
+
 def mlp(oc: OracleCfg, Ws, bs, z, p) -> float:
     W, b = flat_weights(Ws, bs)
     z = _f32(z)
@@ -166,7 +193,7 @@ def rollout(oc: OracleCfg, Ws, bs, z, Tq, x0, goal, U, noise_tk4):
     W, b = flat_weights(Ws, bs)
     T = oc.T
     nz = _f64(noise_tk4)
-    st = np.zeros((T + 1, 10))
+    st = np.zeros((T + 1, 17 if oc.model == 1 else 10))
     q = np.zeros((T, 8))
     s = np.zeros((T, 2))
     c = np.zeros(T)

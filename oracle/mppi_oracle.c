@@ -22,6 +22,12 @@
  *   total cost    J = sum of weighted stage costs                  PAPER.md:185 (Eq. 10), with the
  *                 BASELINE configs[0..1] terms (||p-g_c||^2, 50 exp(-s/0.1), 0.01||u||^2, -0.5 grad s.v)
  *   analytic SDF  s_guide = c + |x| tan(a) - max(|y|,|z|)          PAPER.md:64-72 (Eqs. 1-2)
+ *   paper model   (model 1; SURVEY.md §8f F1 + F2, readings P1-P7)
+ *                 x = [p, v, q, w, T], u = [T1dot..T4dot]            PAPER.md:146 (§IV-A)
+ *                 J_gate = sum_k |p_{k+1}-p_wp|^2 - |p_k-p_wp|^2   PAPER.md:153 (Eq. 6)
+ *                 J_vis  = sum_k 1 - cos(psi_k - psi_gate,k)        PAPER.md:161 (Eq. 7)
+ *                 C_sdf  = max(0, d_safe - s_k), J_sdf = sum_k C   PAPER.md:172, :177 (Eqs. 8-9)
+ *                 J = Q_gate J_gate + Q_vis J_vis + Q_sdf J_sdf     PAPER.md:185 (Eq. 10); Table I
  *   noise RNG     Philox4x32-10 + Box-Muller (reading R24)        — parity unpinned against the paper
  *                 (the paper draws N(0,Sigma) without naming a generator); pinned to the Random123 KAT.
  */
@@ -42,6 +48,11 @@ typedef struct {
     int32_t latent_dim, hidden, n_hidden, activation, mlp_bf16;
     int32_t sdf_mode;            /* 0: MLP g_phi; 1: analytic Gate-SDF (Eq. 2) in the query frame */
     double gate_c, gate_tana;    /* analytic-SDF parameters (sdf_mode 1) */
+    int32_t model;               /* 0: BASELINE CTBR dynamics + configs[0..1] terms; 1: the paper's model */
+    double arm, kappa;           /* model 1: rotor arm (m), yaw moment per unit thrust (m)           */
+    double inertia[3];           /* model 1: diag(J) (kg m^2)                                         */
+    double thrust_max, rate_max; /* model 1: T_i in [0, thrust_max] (N); |w_i| <= rate_max (rad/s)    */
+    double q_gate, q_vis, q_sdf, d_safe;   /* model 1: Eq. 10 weights, Eq. 8 clearance               */
 } oracle_cfg;
 
 /* ------------------------------------------------------------------ Philox4x32-10 (Salmon et al.) */
@@ -142,6 +153,59 @@ void oracle_rk4_step(const double* x, const double* u, double dt, double m, doub
     for (int i = 6; i < 10; ++i) out[i] /= qn;
 }
 
+/* ------------------------------------------------------------------ dynamics (paper model, reading P1-P3) */
+/* x = [p(3), v(3), q(w,x,y,z)(4), w(3) body rates, T(4) rotor thrusts], u = [T1dot..T4dot] (N/s).
+ * pdot = v; vdot = (sum T / m) b3(q) - g e_z; qdot = 1/2 q (x) (0, w); wdot = J^-1 (tau - w x J w);
+ * Tdot = u. X configuration, d = arm / sqrt(2), rotors at body (x, y):
+ * 1 (+d, -d), 2 (-d, +d), 3 (+d, +d), 4 (-d, -d); 1, 2 spin one way and 3, 4 the other:
+ * tau = (sum y_i T_i, -sum x_i T_i, kappa (T1 + T2 - T3 - T4)). */
+void oracle_rotor_deriv(const oracle_cfg* cfg, const double* x, const double* u, double* xd) {
+    const double qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+    const double wx = x[10], wy = x[11], wz = x[12];
+    const double T1 = x[13], T2 = x[14], T3 = x[15], T4 = x[16];
+    const double F = T1 + T2 + T3 + T4;
+    const double d = cfg->arm / sqrt(2.0);
+    xd[0] = x[3]; xd[1] = x[4]; xd[2] = x[5];
+    xd[3] = F / cfg->mass * 2.0 * (qx * qz + qw * qy);
+    xd[4] = F / cfg->mass * 2.0 * (qy * qz - qw * qx);
+    xd[5] = F / cfg->mass * (1.0 - 2.0 * (qx * qx + qy * qy)) - cfg->gravity;
+    xd[6] = 0.5 * (-qx * wx - qy * wy - qz * wz);
+    xd[7] = 0.5 * (qw * wx + qy * wz - qz * wy);
+    xd[8] = 0.5 * (qw * wy + qz * wx - qx * wz);
+    xd[9] = 0.5 * (qw * wz + qx * wy - qy * wx);
+    const double tx = d * (-T1 + T2 + T3 - T4);
+    const double ty = -d * (T1 - T2 + T3 - T4);
+    const double tz = cfg->kappa * (T1 + T2 - T3 - T4);
+    const double Jx = cfg->inertia[0], Jy = cfg->inertia[1], Jz = cfg->inertia[2];
+    /* w x (J w) */
+    const double cx = wy * (Jz * wz) - wz * (Jy * wy);
+    const double cy = wz * (Jx * wx) - wx * (Jz * wz);
+    const double cz = wx * (Jy * wy) - wy * (Jx * wx);
+    xd[10] = (tx - cx) / Jx;
+    xd[11] = (ty - cy) / Jy;
+    xd[12] = (tz - cz) / Jz;
+    for (int i = 0; i < 4; ++i) xd[13 + i] = u[i];
+}
+
+/* RK4 with the input held over the step; then q renormalised, T clamped to [0, thrust_max], w clamped to
+ * +-rate_max (reading P4). */
+void oracle_rotor_step(const oracle_cfg* cfg, const double* x, const double* u, double* out) {
+    const double dt = cfg->dt;
+    double k1[17], k2[17], k3[17], k4[17], xt[17];
+    oracle_rotor_deriv(cfg, x, u, k1);
+    for (int i = 0; i < 17; ++i) xt[i] = x[i] + 0.5 * dt * k1[i];
+    oracle_rotor_deriv(cfg, xt, u, k2);
+    for (int i = 0; i < 17; ++i) xt[i] = x[i] + 0.5 * dt * k2[i];
+    oracle_rotor_deriv(cfg, xt, u, k3);
+    for (int i = 0; i < 17; ++i) xt[i] = x[i] + dt * k3[i];
+    oracle_rotor_deriv(cfg, xt, u, k4);
+    for (int i = 0; i < 17; ++i) out[i] = x[i] + dt / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    double qn = sqrt(out[6] * out[6] + out[7] * out[7] + out[8] * out[8] + out[9] * out[9]);
+    for (int i = 6; i < 10; ++i) out[i] /= qn;
+    for (int i = 10; i < 13; ++i) out[i] = out[i] < -cfg->rate_max ? -cfg->rate_max : (out[i] > cfg->rate_max ? cfg->rate_max : out[i]);
+    for (int i = 13; i < 17; ++i) out[i] = out[i] < 0.0 ? 0.0 : (out[i] > cfg->thrust_max ? cfg->thrust_max : out[i]);
+}
+
 /* ------------------------------------------------------------------ SDF providers */
 static double act_fn(int a, double v) {
     switch (a) {
@@ -220,6 +284,10 @@ void oracle_sdf_rows(const oracle_cfg* cfg, const float* W, const float* b, cons
 }
 
 /* ------------------------------------------------------------------ rollout + cost of one sample */
+static double oracle_rollout_paper(const oracle_cfg* cfg, const float* W, const float* b, const float* z,
+                                   const float* Tq, const float* x0, const float* goal, const float* U,
+                                   const double* noise, int64_t nstride, double* states, double* queries,
+                                   double* sdf, double* stage);
 static double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 /* One sample: u_t = clamp(U*_t + sigma * n_t) (clamp per R5); x_{t+1} = RK4(x_t, u_t);
@@ -233,6 +301,8 @@ static double clampd(double v, double lo, double hi) { return v < lo ? lo : (v >
 double oracle_rollout(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const float* Tq,
                       const float* x0, const float* goal, const float* U, const double* noise, int64_t nstride,
                       double* states, double* queries, double* sdf, double* stage) {
+    if (cfg->model == 1)
+        return oracle_rollout_paper(cfg, W, b, z, Tq, x0, goal, U, noise, nstride, states, queries, sdf, stage);
     const int T = cfg->T;
     double x[10], xn[10], u[4];
     for (int i = 0; i < 10; ++i) x[i] = x0[i];
@@ -269,6 +339,58 @@ double oracle_rollout(const oracle_cfg* cfg, const float* W, const float* b, con
             q[4] = pc2[0]; q[5] = pc2[1]; q[6] = pc2[2]; q[7] = 0.0;
         }
         if (sdf) { sdf[t * 2] = s0; sdf[t * 2 + 1] = s1; }
+        if (stage) stage[t] = ct;
+        J += ct;
+    }
+    if (!isfinite(J)) J = INFINITY;
+    return J;
+}
+
+/* One sample of the paper's model (reading P5-P6): u_k = clamp(U*_k + sigma n_k, +-Tdot_max);
+ * for k = 0..T-1 (the sums of Eqs. 6-9 run over k = 0..K-1 of the current trajectory):
+ *   query the state x_k: p_c = R p_k + t; s_k = g_phi(z, p_c)
+ *   psi_k = yaw of q_k = atan2(2(qw qz + qx qy), 1 - 2(qy^2 + qz^2)); psi_gate,k = atan2(g_y - p_y, g_x - p_x)
+ *   x_{k+1} = step(x_k, u_k)
+ *   c_k = Q_gate (|p_{k+1} - g|^2 - |p_k - g|^2) + Q_vis (1 - cos(psi_k - psi_gate,k)) + Q_sdf max(0, d_safe - s_k)
+ * J = sum_k c_k (non-finite -> +inf). goal = p_wp = the gate centre. Outputs as oracle_rollout, states
+ * [T+1][17]; queries [T][8] = (p_c, |v_k|, 0, 0, 0, 0); sdf [T][2] = (s_k, s_k). */
+static double oracle_rollout_paper(const oracle_cfg* cfg, const float* W, const float* b, const float* z,
+                                   const float* Tq, const float* x0, const float* goal, const float* U,
+                                   const double* noise, int64_t nstride, double* states, double* queries,
+                                   double* sdf, double* stage) {
+    const int T = cfg->T;
+    double x[17], xn[17], u[4];
+    for (int i = 0; i < 17; ++i) x[i] = x0[i];
+    if (states) memcpy(states, x, sizeof(x));
+    double J = 0.0;
+    for (int t = 0; t < T; ++t) {
+        const double* n = noise + (size_t)t * nstride;
+        for (int c = 0; c < 4; ++c) u[c] = clampd((double)U[t * 4 + c] + cfg->sigma[c] * n[c], cfg->u_lo[c], cfg->u_hi[c]);
+        const double* p = x;
+        const double* v = x + 3;
+        double pc[3];
+        for (int r = 0; r < 3; ++r)
+            pc[r] = (double)Tq[r * 3 + 0] * p[0] + (double)Tq[r * 3 + 1] * p[1] + (double)Tq[r * 3 + 2] * p[2] + (double)Tq[9 + r];
+        const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        const double s0 = sdf_eval(cfg, W, b, z, pc);
+        const double qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+        const double psi = atan2(2.0 * (qw * qz + qx * qy), 1.0 - 2.0 * (qy * qy + qz * qz));
+        const double psig = atan2((double)goal[1] - p[1], (double)goal[0] - p[0]);
+        double d0 = 0.0;
+        for (int r = 0; r < 3; ++r) d0 += (p[r] - (double)goal[r]) * (p[r] - (double)goal[r]);
+        oracle_rotor_step(cfg, x, u, xn);
+        double d1 = 0.0;
+        for (int r = 0; r < 3; ++r) d1 += (xn[r] - (double)goal[r]) * (xn[r] - (double)goal[r]);
+        const double hinge = cfg->d_safe - s0 > 0.0 ? cfg->d_safe - s0 : 0.0;
+        const double ct = cfg->q_gate * (d1 - d0) + cfg->q_vis * (1.0 - cos(psi - psig)) + cfg->q_sdf * hinge;
+        memcpy(x, xn, sizeof(x));
+        if (states) memcpy(states + (size_t)(t + 1) * 17, x, sizeof(x));
+        if (queries) {
+            double* q = queries + (size_t)t * 8;
+            q[0] = pc[0]; q[1] = pc[1]; q[2] = pc[2]; q[3] = nv;
+            q[4] = q[5] = q[6] = q[7] = 0.0;
+        }
+        if (sdf) { sdf[t * 2] = s0; sdf[t * 2 + 1] = s0; }
         if (stage) stage[t] = ct;
         J += ct;
     }
@@ -348,7 +470,7 @@ int oracle_combine(const oracle_cfg* cfg, int32_t R, const double* recs, const f
 
 /* ------------------------------------------------------------------ full iteration */
 /* One MPPI iteration for every controller b (already-shifted nominal U). noise: [T][n_ctrl*K][4].
- * Per-controller inputs: z [n][L], Tq [n][12], x0 [n][10], goal [n][3], U [n][T][4].
+ * Per-controller inputs: z [n][L], Tq [n][12], x0 [n][10] (model 1: [n][17]), goal [n][3], U [n][T][4].
  * Optional outputs (NULL to skip): queries [n][K][T][8], sdf [n][K][T][2], stage [n][K][T],
  * J [n][K], Jmin/S/ess [n], V/U_new [n][T][4], flags [n]. */
 void oracle_step(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const float* Tq,
@@ -356,13 +478,14 @@ void oracle_step(const oracle_cfg* cfg, const float* W, const float* b, const fl
                  double* queries, double* sdf, double* stage, double* J, double* Jmin, double* S, double* ess,
                  double* V, double* U_new, int32_t* flags) {
     const int n = cfg->n_ctrl, K = cfg->K, T = cfg->T, L = cfg->latent_dim;
+    const int sd = cfg->model == 1 ? 17 : 10;   /* state dimension */
     const int64_t nstride = (int64_t)n * K * 4;
     double* Jl = J ? J : (double*)malloc(sizeof(double) * (size_t)n * K);
 #pragma omp parallel for schedule(dynamic, 4) collapse(2)
     for (int bb = 0; bb < n; ++bb)
         for (int k = 0; k < K; ++k) {
             size_t sk = (size_t)bb * K + k;
-            Jl[sk] = oracle_rollout(cfg, W, b, z + (size_t)bb * L, Tq + (size_t)bb * 12, x0 + (size_t)bb * 10,
+            Jl[sk] = oracle_rollout(cfg, W, b, z + (size_t)bb * L, Tq + (size_t)bb * 12, x0 + (size_t)bb * sd,
                                     goal + (size_t)bb * 3, U + (size_t)bb * T * 4, noise + sk * 4, nstride, NULL,
                                     queries ? queries + sk * T * 8 : NULL, sdf ? sdf + sk * T * 2 : NULL,
                                     stage ? stage + sk * T : NULL);

@@ -40,14 +40,33 @@ class MPPIConfig:
     steps: int = 1               # closed-loop steps the config asks for (configs[1..]: 100)
     latent_every: int = 0        # redraw latent every N steps (configs[1]: 5)
     per_drone_gates: bool = False  # configs[4]
+    # the paper's own model (model 1; SURVEY.md §8f F1 + F2; readings P1-P7)
+    model: int = 0               # 0: BASELINE CTBR + configs terms; 1: per-rotor thrust-rate model + Eq. 6-10
+    arm: float = 0.15            # P3: rotor arm (m) -- the paper gives no airframe
+    kappa: float = 0.016         # P3: yaw moment per unit thrust (m)
+    inertia: tuple = (0.0025, 0.0025, 0.0045)   # P3: diag(J) (kg m^2)
+    thrust_max: float = 10.0     # Table I "T_s [N] [0, 10]"
+    tdot_max: float = 10.0       # Table I "Tdot_s [-10, 10]"
+    q_gate: float = 1.0          # P6: Eq. 10 weights (the paper gives none)
+    q_vis: float = 2.0
+    q_sdf: float = 10.0
+    d_safe: float = 1.0          # Table I "d_safe 1.0"
 
     @property
     def u_lo(self):
+        if self.model == 1:
+            return (-self.tdot_max,) * 4
         return (0.0, -self.rate_max, -self.rate_max, -self.rate_max)
 
     @property
     def u_hi(self):
+        if self.model == 1:
+            return (self.tdot_max,) * 4
         return (4.0 * self.mass * self.gravity, self.rate_max, self.rate_max, self.rate_max)
+
+    @property
+    def state_dim(self) -> int:
+        return 17 if self.model == 1 else 10
 
     @property
     def fd(self) -> bool:
@@ -87,12 +106,21 @@ CONFIGS = {
                      w_guide=0.5, steps=100, per_drone_gates=True),
 }
 
+# The paper's configuration (SURVEY.md §8f F1 + F2): Table I M=8192, K=20, dt=0.03,
+# lambda in [0.01, 0.1], Tdot in [-10, 10], T in [0, 10] N, w in [-10, 10] rad/s, d_safe = 1; latent
+# z in R^128; the per-rotor thrust-rate model and Eq. 6-10 costs; MLP size unstated ->
+# the configs[2] MLP; no guidance term (Eq. 10 has none).
+CONFIGS["c5"] = MPPIConfig(name="c5", model=1, K=8192, T=20, dt=0.03, lam=0.05, rate_max=10.0,
+                           sigma=(5.0, 5.0, 5.0, 5.0), latent_dim=128, hidden=256, n_hidden=4,
+                           activation=ACT_SILU, mlp_dtype=MLP_BF16, w_guide=0.0, steps=100, latent_every=5)
+
 # Reduced parity variants: same MLP/cost/dynamics structure, sizes the oracle finishes in seconds
 # while still spanning several 128-row tiles and a ragged tail.
 CONFIGS["c1s"] = CONFIGS["c1"].replace(name="c1s", K=200, T=7, steps=1)
 CONFIGS["c2s"] = CONFIGS["c2"].replace(name="c2s", K=136, T=5, steps=1)
 CONFIGS["c3s"] = CONFIGS["c3"].replace(name="c3s", K=256, T=6, steps=1)
 CONFIGS["c4s"] = CONFIGS["c4"].replace(name="c4s", n_ctrl=6, K=64, T=4, steps=1)
+CONFIGS["c5s"] = CONFIGS["c5"].replace(name="c5s", K=200, T=6, steps=1)
 
 
 def get_config(name: str, **overrides) -> MPPIConfig:

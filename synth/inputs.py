@@ -85,9 +85,12 @@ def make_query_transforms(cfg: MPPIConfig, seed: int | None = None) -> np.ndarra
 
 
 def make_x0(cfg: MPPIConfig, jitter: float = 0.0, seed: int | None = None) -> np.ndarray:
-    """[n_ctrl][10] float32: p=0, v=0, q=(1,0,0,0) (R18); optional seeded jitter on p, v."""
-    x0 = np.zeros((cfg.n_ctrl, 10), np.float32)
+    """[n_ctrl][10] float32: p=0, v=0, q=(1,0,0,0) (R18); optional seeded jitter on p, v.
+    Paper model (cfg.model == 1): [n_ctrl][17], also w = 0 and hover rotor thrusts T_i = m g / 4 (P7)."""
+    x0 = np.zeros((cfg.n_ctrl, cfg.state_dim), np.float32)
     x0[:, 6] = 1.0
+    if cfg.model == 1:
+        x0[:, 13:17] = np.float32(cfg.mass * cfg.gravity / 4.0)
     if jitter:
         rng = rng_for(cfg.seed if seed is None else seed, "x0")
         x0[:, 0:6] += rng.uniform(-jitter, jitter, size=(cfg.n_ctrl, 6)).astype(np.float32)
@@ -95,9 +98,11 @@ def make_x0(cfg: MPPIConfig, jitter: float = 0.0, seed: int | None = None) -> np
 
 
 def make_nominal(cfg: MPPIConfig) -> np.ndarray:
-    """[n_ctrl][T][4] float32 hover nominal: thrust m*g, zero body rates (R18)."""
+    """[n_ctrl][T][4] float32 hover nominal: thrust m*g, zero body rates (R18). Paper model: zero thrust
+    rates (the hover thrusts are in the state)."""
     U = np.zeros((cfg.n_ctrl, cfg.T, 4), np.float32)
-    U[:, :, 0] = np.float32(cfg.mass * cfg.gravity)
+    if cfg.model == 0:
+        U[:, :, 0] = np.float32(cfg.mass * cfg.gravity)
     return U
 
 
