@@ -13,7 +13,8 @@
  * ("latent duplicated M x K times and concatenated", folded; "encode ... once").
  *
  * Conventions: all arrays are little-endian, row-major, fp32 unless stated. State x = [p(3), v(3),
- * q(w,x,y,z)]; control u = [c (N), wx, wy, wz (rad/s, body frame)]; MLP weights in nn.Linear order
+ * q(w,x,y,z)]; control u = [c (N), wx, wy, wz (rad/s, body frame)] (MPPI_MODEL_PAPER: see below; the
+ * state dimension is 17 and u is the rotor thrust rates); MLP weights in nn.Linear order
  * W[out][in], layer-1 input columns [p_c(3) | z(L)]. Units: m, s, N, rad.
  *
  * Ownership: the caller owns the device workspace (>= mppi_workspace_bytes()) and must keep it alive
@@ -37,7 +38,7 @@
 extern "C" {
 #endif
 
-#define MPPI_ABI_VERSION 1
+#define MPPI_ABI_VERSION 2
 
 typedef struct mppi_ctx mppi_ctx;
 typedef int32_t mppi_status;
@@ -56,6 +57,15 @@ enum {
 enum { MPPI_ACT_SOFTPLUS = 0, MPPI_ACT_RELU = 1, MPPI_ACT_SILU = 2 };
 enum { MPPI_MLP_FP32 = 0, MPPI_MLP_BF16 = 1 };
 enum { MPPI_NOISE_DEVICE = 0, MPPI_NOISE_EXTERNAL = 1 };
+/* MPPI_MODEL_BASELINE: the CTBR dynamics and cost terms of BASELINE configs[0..4] (above).
+ * MPPI_MODEL_PAPER: the paper's own model (SURVEY.md §8f F1 + F2; readings P1-P7):
+ *   state x = [p(3), v(3), q(w,x,y,z)(4), w(3) body rates, T(4) rotor thrusts] (17 floats),
+ *   control u = [T1dot..T4dot] (N/s), X-configuration rigid body, RK4 with T clamped to
+ *   [0, thrust_max] and w to +-rate_max after each step;
+ *   J = sum_{k=0}^{T-1} q_gate (|p_{k+1} - g|^2 - |p_k - g|^2) + q_vis (1 - cos(psi_k - psi_gate,k))
+ *       + q_sdf max(0, d_safe - s(p_k))                      (Eqs. 6-10),
+ *   so the SDF is queried at x_0..x_{T-1}; w_goal, w_sdf, sdf_scale, w_u are unused and w_guide must be 0. */
+enum { MPPI_MODEL_BASELINE = 0, MPPI_MODEL_PAPER = 1 };
 
 typedef struct {
     int32_t abi_version;       /* MPPI_ABI_VERSION                                                 */
@@ -76,6 +86,12 @@ typedef struct {
                                                    Non-NULL also with world_size 1 (exercises the path) */
     int32_t device;                             /* CUDA device ordinal                              */
     void* stream;                               /* cudaStream_t all work is enqueued on (0: legacy) */
+    /* ABI 2 */
+    int32_t model;                              /* MPPI_MODEL_*                                     */
+    float arm, kappa;                           /* MPPI_MODEL_PAPER: rotor arm (m), yaw moment per thrust (m) */
+    float inertia[3];                           /* MPPI_MODEL_PAPER: diag(J) (kg m^2)               */
+    float thrust_max, rate_max;                 /* MPPI_MODEL_PAPER: rotor thrust (N), body-rate (rad/s) limits */
+    float q_gate, q_vis, q_sdf, d_safe;         /* MPPI_MODEL_PAPER: Eq. 10 weights, Eq. 8 clearance (m) */
 } mppi_config;
 
 /* Bytes of device workspace mppi_create() needs for this config (0 if the config is invalid). */
@@ -109,7 +125,8 @@ mppi_status mppi_set_nominal(mppi_ctx* ctx, int32_t ctrl, const float* U);
  * Each step uses the last noise set (sigma is applied inside the step). */
 mppi_status mppi_set_noise(mppi_ctx* ctx, const float* d_noise);
 
-/* One MPPI iteration. x0 [n_ctrl][10], goal g_c [n_ctrl][3] are HOST arrays. If step_index > 0 the
+/* One MPPI iteration. x0 [n_ctrl][10] (MPPI_MODEL_PAPER: [n_ctrl][17]), goal g_c [n_ctrl][3] (the
+ * paper model's waypoint p_wp) are HOST arrays. If step_index > 0 the
  * nominal is first shifted (U*_t <- U*_{t+1}, last repeated). step_index also keys the
  * device noise. world_size > 1 with NCCL: includes the all-gather + combine; without NCCL the caller
  * uses mppi_step_local / mppi_step_finish. Async; returns MPPI_ERR_NOT_READY before weights/latents. */

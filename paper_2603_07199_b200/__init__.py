@@ -58,6 +58,7 @@ class Controller:
         _lib._check(self.lib.mppi_create(C.byref(self.c), C.c_void_p(self.ws_ptr), nbytes, C.byref(self.ctx)))
         self.n, self.K, self.T = cfg.n_ctrl, cfg.K, cfg.T
         self.rps = 2 if cfg.w_guide != 0 else 1
+        self.state_dim = 17 if getattr(cfg, "model", 0) == 1 else 10
         if debug_outputs:
             self.set_debug_outputs(True)
 
@@ -106,18 +107,23 @@ class Controller:
         _lib._check(self.lib.mppi_set_noise(self.ctx, C.c_void_p(noise.data_ptr())))
 
     # ---------------------------------------------------------------- steps
+    def _host_inputs(self, x0, goal):
+        x0, goal = _f32(x0), _f32(goal)
+        if x0.size != self.n * self.state_dim or goal.size != self.n * 3:
+            raise ValueError(f"x0 must be [{self.n}][{self.state_dim}] and goal [{self.n}][3]")
+        return x0, goal
+
     def step(self, x0, goal, step_index: int = 0):
-        x0 = _f32(x0)
-        goal = _f32(goal)
+        x0, goal = self._host_inputs(x0, goal)
         _lib._check(self.lib.mppi_step(self.ctx, _lib._ptr(x0), _lib._ptr(goal), step_index))
 
     def step_device(self, x0, goal, step_index: int = 0):
-        """x0, goal: torch CUDA float32 tensors [n_ctrl][10], [n_ctrl][3]."""
+        """x0, goal: torch CUDA float32 tensors [n_ctrl][10] ([n_ctrl][17] for the paper model), [n_ctrl][3]."""
         _lib._check(self.lib.mppi_step_device(self.ctx, C.c_void_p(x0.data_ptr()), C.c_void_p(goal.data_ptr()),
                                               step_index))
 
     def step_local(self, x0, goal, step_index: int = 0):
-        x0 = _f32(x0)
+        x0, goal = self._host_inputs(x0, goal)
         goal = _f32(goal)
         _lib._check(self.lib.mppi_step_local(self.ctx, _lib._ptr(x0), _lib._ptr(goal), step_index))
 

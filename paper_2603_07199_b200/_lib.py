@@ -11,7 +11,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmppi_b200.so")
 
-MPPI_ABI_VERSION = 1
+MPPI_ABI_VERSION = 2
 STATUS = {0: "OK", -1: "INVALID", -2: "CUDA", -3: "NCCL", -4: "NOT_READY", -5: "NONFINITE", -6: "OOM",
           -7: "POISONED", -8: "UNSUPPORTED"}
 MPPI_OK, MPPI_ERR_INVALID, MPPI_ERR_NONFINITE, MPPI_ERR_UNSUPPORTED = 0, -1, -5, -8
@@ -44,6 +44,10 @@ class MppiConfig(C.Structure):
         ("activation", C.c_int32), ("mlp_dtype", C.c_int32), ("noise_mode", C.c_int32),
         ("seed", C.c_uint64), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("stream", C.c_void_p),
+        # ABI 2
+        ("model", C.c_int32), ("arm", C.c_float), ("kappa", C.c_float), ("inertia", C.c_float * 3),
+        ("thrust_max", C.c_float), ("rate_max", C.c_float),
+        ("q_gate", C.c_float), ("q_vis", C.c_float), ("q_sdf", C.c_float), ("d_safe", C.c_float),
     ]
 
 
@@ -129,4 +133,10 @@ def make_config(cfg, *, device: int = 0, stream: int = 0, noise_mode: str = "dev
         c.nccl_unique_id = C.cast(c._nccl_buf, C.c_void_p)
     c.device = device
     c.stream = stream
+    c.model = getattr(cfg, "model", 0)
+    if c.model == 1:
+        c.arm, c.kappa, c.thrust_max, c.rate_max = cfg.arm, cfg.kappa, cfg.thrust_max, cfg.rate_max
+        for i in range(3):
+            c.inertia[i] = cfg.inertia[i]
+        c.q_gate, c.q_vis, c.q_sdf, c.d_safe = cfg.q_gate, cfg.q_vis, cfg.q_sdf, cfg.d_safe
     return c

@@ -622,7 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                            p.w_guide * row_of(i).w * (s1 - sv) * p.inv_fd_h;
                         if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
                     } else {
-                        const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
+                        const float term = p.model == MPPI_MODEL_PAPER
+                                               ? p.q_sdf * fmaxf(p.d_safe - sv, 0.f)   // Eq. 8 hinge
+                                               : p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max));
                         if (row < n_rows) terms[row] = term;
                     }
                 }

@@ -191,8 +191,129 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
     b.partial[col] = part;
 }
 
+// ------------------------------------------------------------------ K1 (paper model): rotor rollout
+// MPPI_MODEL_PAPER (SURVEY.md §8f F1 + F2; readings P1-P6): x = [p, v, q, w, T], u = Tdot;
+// pdot = v; vdot = (sum T / m) b3(q) - g e_z; qdot = 1/2 q (x) (0, w); wdot = J^-1 (tau - w x J w); Tdot = u
+// (PAPER.md:146), X mixer tau = (d(-T1 + T2 + T3 - T4), -d(T1 - T2 + T3 - T4), kappa (T1 + T2 - T3 - T4)).
+__device__ __forceinline__ void dyn_rotor(const Params& p, const float* x, const float* u, float* xd) {
+    const float qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+    const float wx = x[10], wy = x[11], wz = x[12];
+    const float T1 = x[13], T2 = x[14], T3 = x[15], T4 = x[16];
+    const float fm = (T1 + T2 + T3 + T4) / p.mass;
+    xd[0] = x[3]; xd[1] = x[4]; xd[2] = x[5];
+    xd[3] = fm * (2.f * (qx * qz + qw * qy));
+    xd[4] = fm * (2.f * (qy * qz - qw * qx));
+    xd[5] = fm * (1.f - 2.f * (qx * qx + qy * qy)) - p.gravity;
+    xd[6] = 0.5f * (-qx * wx - qy * wy - qz * wz);
+    xd[7] = 0.5f * (qw * wx + qy * wz - qz * wy);
+    xd[8] = 0.5f * (qw * wy + qz * wx - qx * wz);
+    xd[9] = 0.5f * (qw * wz + qx * wy - qy * wx);
+    const float tx = p.arm_d * (-T1 + T2 + T3 - T4);
+    const float ty = -p.arm_d * (T1 - T2 + T3 - T4);
+    const float tz = p.kappa * (T1 + T2 - T3 - T4);
+    xd[10] = (tx - (wy * (p.Jz * wz) - wz * (p.Jy * wy))) * p.inv_Jx;
+    xd[11] = (ty - (wz * (p.Jx * wx) - wx * (p.Jz * wz))) * p.inv_Jy;
+    xd[12] = (tz - (wx * (p.Jy * wy) - wy * (p.Jx * wx))) * p.inv_Jz;
+    xd[13] = u[0]; xd[14] = u[1]; xd[15] = u[2]; xd[16] = u[3];
+}
+
+// One thread per (controller, sample). Per step k = 0..T-1 (the sums of Eqs. 6-9 run over the states
+// x_0..x_{T-1}): the query row of x_k (p_c = R p_k + t, |v_k|), the yaw-alignment term of x_k, the RK4
+// step to x_{k+1} (then q renormalised, w and T clamped; reading P4) and the progress term
+// |p_{k+1} - g|^2 - |p_k - g|^2. The SDF hinge term q_sdf max(0, d_safe - s) is added by the MLP kernel.
+template <bool DEV>
+__global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffers b) {
+    __shared__ float4 s_U[kMaxTStaged];
+    const int bb = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long step = *b.step;
+    const int sh = step > 0 ? 1 : 0;
+    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+        const float4 u = reinterpret_cast<const float4*>(b.U_out)[(long long)bb * p.T + min(t + sh, p.T - 1)];
+        if (t < kMaxTStaged) s_U[t] = u;
+        if (blockIdx.x == 0) reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] = u;
+    }
+    __syncthreads();
+    if (k >= p.K) return;
+    float x[17];
+#pragma unroll
+    for (int i = 0; i < 17; ++i) x[i] = __ldg(b.x0 + bb * 17 + i);
+    const float* Tq = b.Tq + bb * 12;
+    float R[9], tq[3], gc[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = __ldg(Tq + i);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { tq[i] = __ldg(Tq + 9 + i); gc[i] = __ldg(b.goal + bb * 3 + i); }
+    const float4* Uo = reinterpret_cast<const float4*>(b.U_out) + (long long)bb * p.T;
+    auto nominal = [&](int t) { return t < kMaxTStaged ? s_U[t] : Uo[min(t + sh, p.T - 1)]; };
+    const long long NK = (long long)p.n_ctrl * p.K;
+    const long long col = (long long)bb * p.K + k;
+    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f;
+    float part = 0.f;
+    float4 n_next = DEV ? philox_normals(gidx, 0, step, p.seed) : b.noise[col];
+    float4 U_next = nominal(0);
+    for (int t = 0; t < p.T; ++t) {
+        const float4 n = n_next;
+        const float4 U = U_next;
+        if (DEV) b.noise[(long long)t * NK + col] = n;
+        if (t + 1 < p.T) {
+            n_next = DEV ? philox_normals(gidx, t + 1, step, p.seed) : b.noise[(long long)(t + 1) * NK + col];
+            U_next = nominal(t + 1);
+        }
+        float u[4];
+        u[0] = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
+        u[1] = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
+        u[2] = clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]);
+        u[3] = clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]);
+        // ---- query row and yaw alignment of x_k
+        float pc[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) pc[r] = R[3 * r] * x[0] + R[3 * r + 1] * x[1] + R[3 * r + 2] * x[2] + tq[r];
+        const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+        b.rows[((long long)bb * p.T + t) * p.K + k] = make_float4(pc[0], pc[1], pc[2], nv);
+        // cos(psi - psi_gate) as the dot of unit heading and line-of-sight vectors (atan2(0,0) = 0 -> (1,0))
+        const float hx = 1.f - 2.f * (x[8] * x[8] + x[9] * x[9]), hy = 2.f * (x[6] * x[9] + x[7] * x[8]);
+        const float lx = gc[0] - x[0], ly = gc[1] - x[1];
+        const float h2 = hx * hx + hy * hy, l2 = lx * lx + ly * ly;
+        const float hi = h2 > 0.f ? rsqrtf(h2) : 0.f, li = l2 > 0.f ? rsqrtf(l2) : 0.f;
+        const float chx = h2 > 0.f ? hx * hi : 1.f, chy = hy * hi, clx = l2 > 0.f ? lx * li : 1.f, cly = ly * li;
+        const float vis = 1.f - (chx * clx + chy * cly);
+        const float d0 = (x[0] - gc[0]) * (x[0] - gc[0]) + (x[1] - gc[1]) * (x[1] - gc[1]) + (x[2] - gc[2]) * (x[2] - gc[2]);
+        // ---- RK4 step (input held), running sum of the stage derivatives
+        float kk[17], acc[17], xt[17];
+        dyn_rotor(p, x, u, kk);
+#pragma unroll
+        for (int i = 0; i < 17; ++i) { acc[i] = kk[i]; xt[i] = x[i] + hdt * kk[i]; }
+        dyn_rotor(p, xt, u, kk);
+#pragma unroll
+        for (int i = 0; i < 17; ++i) { acc[i] += 2.f * kk[i]; xt[i] = x[i] + hdt * kk[i]; }
+        dyn_rotor(p, xt, u, kk);
+#pragma unroll
+        for (int i = 0; i < 17; ++i) { acc[i] += 2.f * kk[i]; xt[i] = x[i] + dt * kk[i]; }
+        dyn_rotor(p, xt, u, kk);
+#pragma unroll
+        for (int i = 0; i < 17; ++i) x[i] = x[i] + dt6 * (acc[i] + kk[i]);
+        const float qinv = rsqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);
+#pragma unroll
+        for (int i = 6; i < 10; ++i) x[i] *= qinv;
+#pragma unroll
+        for (int i = 10; i < 13; ++i) x[i] = clampf(x[i], -p.rate_max, p.rate_max);
+#pragma unroll
+        for (int i = 13; i < 17; ++i) x[i] = clampf(x[i], 0.f, p.thrust_max);
+        const float d1 = (x[0] - gc[0]) * (x[0] - gc[0]) + (x[1] - gc[1]) * (x[1] - gc[1]) + (x[2] - gc[2]) * (x[2] - gc[2]);
+        part += p.q_gate * (d1 - d0) + p.q_vis * vis;
+    }
+    b.partial[col] = part;
+}
+
 void launch_rollout(const Params& p, const Buffers& b, bool device_noise, cudaStream_t s) {
     dim3 grid((p.K + kRolloutBlock - 1) / kRolloutBlock, p.n_ctrl);
+    if (p.model == MPPI_MODEL_PAPER) {
+        if (device_noise) k_rollout_paper<true><<<grid, kRolloutBlock, 0, s>>>(p, b);
+        else k_rollout_paper<false><<<grid, kRolloutBlock, 0, s>>>(p, b);
+        return;
+    }
     if (device_noise) k_rollout<true><<<grid, kRolloutBlock, 0, s>>>(p, b);
     else k_rollout<false><<<grid, kRolloutBlock, 0, s>>>(p, b);
 }
@@ -254,8 +375,13 @@ __global__ void __launch_bounds__(128) k_mlp_simt(Params p, Buffers b, const flo
         if (sdf_out) sdf_out[i * rps + r] = sv[r];
     }
     if (states_mode) {
-        float term = p.w_sdf * expf(fminf(-sv[0] * p.inv_sdf_scale, p.sdf_exp_max));
-        if (rps == 2) term -= p.w_guide * nv * (sv[1] - sv[0]) * p.inv_fd_h;
+        float term;
+        if (p.model == MPPI_MODEL_PAPER) {
+            term = p.q_sdf * fmaxf(p.d_safe - sv[0], 0.f);   // Eq. 8 hinge
+        } else {
+            term = p.w_sdf * expf(fminf(-sv[0] * p.inv_sdf_scale, p.sdf_exp_max));
+            if (rps == 2) term -= p.w_guide * nv * (sv[1] - sv[0]) * p.inv_fd_h;
+        }
         b.terms[i] = term;
     }
 }

@@ -56,7 +56,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_BOUT] = 16;
     sz[B_Z] = 4 * n * Ld;
     sz[B_TQ] = 4 * n * 12;
-    sz[B_X0] = 4 * n * 10;
+    sz[B_X0] = 4 * n * (c->model == MPPI_MODEL_PAPER ? 17 : 10);
     sz[B_GOAL] = 4 * n * 3;
     sz[B_STEP] = 16;
     sz[B_UOUT] = 16 * n * T;
@@ -145,6 +145,8 @@ struct mppi_ctx {
         }                                                                                               \
     } while (0)
 
+static int state_dim(const mppi_config* c) { return c->model == MPPI_MODEL_PAPER ? 17 : 10; }
+
 static mppi_status validate(const mppi_config* c) {
     if (!c) return fail(MPPI_ERR_INVALID, "cfg is NULL");
     if (c->abi_version != MPPI_ABI_VERSION) return fail(MPPI_ERR_INVALID, "abi_version mismatch");
@@ -154,6 +156,15 @@ static mppi_status validate(const mppi_config* c) {
     if (!(c->dt > 0.f) || !(c->lambda > 0.f) || !(c->mass > 0.f)) return fail(MPPI_ERR_INVALID, "dt, lambda, mass > 0");
     if (!(c->sdf_scale > 0.f)) return fail(MPPI_ERR_INVALID, "sdf_scale > 0");
     if (c->w_guide != 0.f && !(c->fd_h > 0.f)) return fail(MPPI_ERR_INVALID, "fd_h > 0 with guidance");
+    if (c->model != MPPI_MODEL_BASELINE && c->model != MPPI_MODEL_PAPER) return fail(MPPI_ERR_INVALID, "bad model");
+    if (c->model == MPPI_MODEL_PAPER) {
+        if (c->w_guide != 0.f) return fail(MPPI_ERR_INVALID, "the paper model has no guidance term (w_guide must be 0)");
+        if (!(c->inertia[0] > 0.f) || !(c->inertia[1] > 0.f) || !(c->inertia[2] > 0.f) || !(c->arm > 0.f))
+            return fail(MPPI_ERR_INVALID, "inertia and arm must be > 0");
+        if (!(c->thrust_max > 0.f) || !(c->rate_max > 0.f)) return fail(MPPI_ERR_INVALID, "thrust_max, rate_max > 0");
+        if (!std::isfinite(c->q_gate) || !std::isfinite(c->q_vis) || !std::isfinite(c->q_sdf) || !std::isfinite(c->d_safe))
+            return fail(MPPI_ERR_INVALID, "non-finite cost weight");
+    }
     for (int i = 0; i < 4; ++i)
         if (!(c->u_lo[i] <= c->u_hi[i])) return fail(MPPI_ERR_INVALID, "u_lo > u_hi");
     if (c->latent_dim < 0 || c->hidden < 1 || c->n_hidden < 1) return fail(MPPI_ERR_INVALID, "bad MLP dims");
@@ -259,6 +270,13 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.sdf_exp_max = cfg->sdf_exp_max; p.w_u = cfg->w_u; p.w_guide = cfg->w_guide; p.fd_h = cfg->fd_h;
     p.inv_fd_h = cfg->fd_h > 0.f ? 1.f / cfg->fd_h : 0.f;
     p.seed = cfg->seed;
+    p.model = cfg->model;
+    p.arm_d = cfg->arm / sqrtf(2.f);
+    p.kappa = cfg->kappa;
+    p.Jx = cfg->inertia[0]; p.Jy = cfg->inertia[1]; p.Jz = cfg->inertia[2];
+    p.inv_Jx = 1.f / cfg->inertia[0]; p.inv_Jy = 1.f / cfg->inertia[1]; p.inv_Jz = 1.f / cfg->inertia[2];
+    p.thrust_max = cfg->thrust_max; p.rate_max = cfg->rate_max;
+    p.q_gate = cfg->q_gate; p.q_vis = cfg->q_vis; p.q_sdf = cfg->q_sdf; p.d_safe = cfg->d_safe;
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
     ctx->latent_set.assign(cfg->n_ctrl, 0);
 
@@ -266,7 +284,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         mppi_destroy(ctx);
         return fail(s, m);
     };
-    const size_t stage_floats = (size_t)cfg->n_ctrl * 13 + 4;
+    const size_t stage_floats = (size_t)cfg->n_ctrl * (state_dim(cfg) + 3) + 4;
     for (int i = 0; i < kStaging; ++i) {
         if (cudaHostAlloc((void**)&ctx->h_stage[i], stage_floats * sizeof(float), cudaHostAllocDefault) != cudaSuccess)
             return cleanup(MPPI_ERR_OOM, "cudaHostAlloc staging");
@@ -471,7 +489,7 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     if (!x0 || !goal) return fail(MPPI_ERR_INVALID, "NULL x0/goal");
     if (mode == 0 && ctx->cfg.world_size > 1 && !ctx->comm)
         return fail(MPPI_ERR_INVALID, "sharded context without NCCL: use mppi_step_local / mppi_step_finish");
-    const int n = ctx->cfg.n_ctrl;
+    const int n = ctx->cfg.n_ctrl, sd = state_dim(&ctx->cfg);
     // The graph runs on the internal stream, ordered after everything already queued on the caller's
     // stream; the caller's stream then waits for the step (so setters, debug copies and
     // get_controls on cfg.stream see its results).
@@ -479,21 +497,21 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in, ctx->stream));
     CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_in, 0));
     if (device_inputs) {
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, x0, sizeof(float) * n * 10, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, x0, sizeof(float) * n * sd, cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, goal, sizeof(float) * n * 3, cudaMemcpyDeviceToDevice, s));
-        unsigned long long* hs = reinterpret_cast<unsigned long long*>(ctx->h_stage[ctx->stage_i] + (size_t)n * 13);
+        unsigned long long* hs = reinterpret_cast<unsigned long long*>(ctx->h_stage[ctx->stage_i] + (size_t)n * (sd + 3));
         CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));
         *hs = step;
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, hs, 8, cudaMemcpyHostToDevice, s));
     } else {
         float* h = ctx->h_stage[ctx->stage_i];
         CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));   // previous use of this slot done
-        std::memcpy(h, x0, sizeof(float) * n * 10);
-        std::memcpy(h + n * 10, goal, sizeof(float) * n * 3);
-        *reinterpret_cast<unsigned long long*>(h + (size_t)n * 13) = step;
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, h, sizeof(float) * n * 10, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, h + n * 10, sizeof(float) * n * 3, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, h + (size_t)n * 13, 8, cudaMemcpyHostToDevice, s));
+        std::memcpy(h, x0, sizeof(float) * n * sd);
+        std::memcpy(h + (size_t)n * sd, goal, sizeof(float) * n * 3);
+        *reinterpret_cast<unsigned long long*>(h + (size_t)n * (sd + 3)) = step;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, h, sizeof(float) * n * sd, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, h + (size_t)n * sd, sizeof(float) * n * 3, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, h + (size_t)n * (sd + 3), 8, cudaMemcpyHostToDevice, s));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->stage_ev[ctx->stage_i], s));
     ctx->stage_i = (ctx->stage_i + 1) % kStaging;

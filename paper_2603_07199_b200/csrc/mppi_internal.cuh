@@ -18,6 +18,11 @@ struct Params {
     float u_lo[4], u_hi[4], sigma[4];
     float w_goal, w_sdf, inv_sdf_scale, sdf_exp_max, w_u, w_guide, fd_h, inv_fd_h;
     unsigned long long seed;
+    // MPPI_MODEL_PAPER (reading P1-P6)
+    int model;
+    float arm_d, kappa;              // arm / sqrt(2) (rotor offset along each body axis), yaw moment per thrust
+    float Jx, Jy, Jz, inv_Jx, inv_Jy, inv_Jz;
+    float thrust_max, rate_max, q_gate, q_vis, q_sdf, d_safe;
 };
 
 // Device buffers of one context (all inside the workspace).

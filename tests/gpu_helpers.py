@@ -70,6 +70,9 @@ def sdf_tol(cfg, s_ref):
 def cost_tol(cfg, ref, tol_s):
     """Propagate the SDF tolerance through the stage cost:
     |dJ| <= 1e-5 sum_t |c_t| + sum_t [w_sdf/scale e^{-s/scale} + 2 w_guide |v| / h] tol_s."""
+    if getattr(cfg, "model", 0) == 1:
+        # paper model: the hinge q_sdf max(0, d_safe - s) is 1-Lipschitz in s
+        return 1e-5 * np.abs(ref["stage"]).sum(-1) + (cfg.q_sdf * np.broadcast_to(tol_s, ref["stage"].shape)).sum(-1) + 1e-6
     s0 = ref["sdf"][..., 0]
     nv = ref["queries"][..., 3]
     e = np.exp(np.minimum(-s0 / cfg.sdf_scale, cfg.sdf_exp_max))

@@ -394,3 +394,58 @@ def test_nccl_exchange_path_single_rank():
         c.close()
     assert outs[1][1] == outs[0][1] + 1     # + k_combine
     np.testing.assert_allclose(outs[1][0], outs[0][0], atol=1e-5)
+
+
+# ---------------------------------------------------------------- the paper's model (SURVEY §8f F1 + F2)
+
+def test_paper_model_step_parity():
+    """configs c5s (per-rotor thrust-rate dynamics, Eq. 6-10 costs): query rows at x_0..x_{T-1}, SDF
+    rows, costs and the update against the oracle on the same external noise."""
+    cfg, Ws, bs, inp, ctrl = gh.setup("c5s")
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
+    # the non-SDF part (progress + alignment) is fp32 arithmetic on fp32 states: tight
+    part = ctrl.debug("partial").astype(np.float64)
+    want = ref["stage"].sum(-1) - cfg.q_sdf * np.maximum(cfg.d_safe - ref["sdf"][..., 0], 0.0).sum(-1)
+    ok, err = _close(part, want, 1e-5, 1e-4)
+    assert ok, err
+
+
+def test_paper_model_zero_noise_keeps_nominal_on_gpu():
+    cfg, Ws, bs, inp, ctrl = gh.setup("c5s", noise_mode="external")
+    U = inp["U"] + np.float32(0.5)
+    ctrl.set_nominal(U)
+    ctrl.set_noise(np.zeros_like(np.asarray(inp["noise"])))
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    Ug, _ = ctrl.get_controls()
+    np.testing.assert_allclose(Ug, U, atol=1e-6)
+
+
+def test_paper_model_full_size_sampled_parity():
+    """configs c5 (Table I scale: K=8192, T=20, dt=0.03) with device noise: sampled rollouts recomputed
+    one by one by the oracle; the update checked by the softmin property on the GPU's own costs."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config("c5")
+    Ws, bs = synth.make_weights(cfg)
+    z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
+                          synth.make_goals(cfg), synth.make_nominal(cfg))
+    ctrl = Controller(cfg, noise_mode="device", debug_outputs=True)
+    ctrl.set_sdf_weights(Ws, bs)
+    ctrl.set_latent(z, Tq)
+    ctrl.set_nominal(U)
+    ctrl.step(x0, goal, 4)
+    Ug, _ = ctrl.get_controls()
+    J = ctrl.debug("costs").astype(np.float64)
+    sdf = ctrl.debug("sdf")
+    oc = oracle.make_cfg(cfg)
+    for k in np.random.default_rng(2).choice(cfg.K, size=8, replace=False):
+        nz = oracle.noise(cfg.seed, 4, int(k), 1, cfg.T)[:, 0, :]
+        r = oracle.rollout(oc, Ws, bs, z[0], Tq[0], x0[0], goal[0], U[0], nz)
+        assert np.abs(sdf[0, :, k, 0] - r["sdf"][:, 0]).max() <= gh.ABS_SDF_BF16
+        ref = {"stage": r["stage"][None], "sdf": r["sdf"][None], "queries": r["queries"][None]}
+        tol = gh.cost_tol(cfg, ref, gh.ABS_SDF_BF16)[0]
+        assert abs(J[0, k] - r["J"]) <= tol, (J[0, k], r["J"], tol)
+    noise = oracle.noise(cfg.seed, 4, 0, cfg.K, cfg.T)
+    prop = gh.softmin_property(cfg, U[0], noise, J[0])
+    assert np.abs(Ug[0] - prop).max() <= gh.ABS_U
