@@ -101,16 +101,46 @@ __device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, fl
 
 constexpr int kRolloutBlock = 64;   // small blocks: K/64 blocks spread the latency-bound rollout over all SMs
 
+// Device-noise producer warps of a rollout block (DEV): they generate the Philox normals of step t+1
+// (and store them for k_softmin) while the consumer warps integrate step t, handing them over through a
+// two-slot shared-memory buffer with one named barrier per step -- the Philox + Box-Muller chain is
+// off the rollout's dependency chain (measured: the inline form cost ~10 us per step at configs[1..2]).
+__device__ __forceinline__ void named_sync_rollout() {
+    asm volatile("bar.sync 1, %0;" ::"r"(2 * kRolloutBlock) : "memory");
+}
+__device__ void rollout_noise_producer(const Params& p, const Buffers& b, int bb, int lt, int k,
+                                       unsigned long long step, float4 (*s_n)[kRolloutBlock]) {
+    const bool valid = k < p.K;
+    const long long NK = (long long)p.n_ctrl * p.K, col = (long long)bb * p.K + k;
+    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+    if (valid) {
+        const float4 n = philox_normals(gidx, 0, step, p.seed);
+        s_n[0][lt] = n;
+        b.noise[col] = n;
+    }
+    named_sync_rollout();
+    for (int t = 0; t < p.T; ++t) {
+        if (valid && t + 1 < p.T) {
+            const float4 n = philox_normals(gidx, t + 1, step, p.seed);
+            s_n[(t + 1) & 1][lt] = n;
+            b.noise[(long long)(t + 1) * NK + col] = n;
+        }
+        named_sync_rollout();
+    }
+}
+
 // DEV: generate the noise in registers (Philox, one step ahead) and store it for k_softmin; otherwise
 // read the externally set noise. The warm-start shift is fused: the nominal is read from U_out at the
 // shifted index, and block 0 of each controller writes the shifted copy U_nom for k_softmin.
 constexpr int kMaxTStaged = 128;   // nominal staged in shared memory up to this horizon
 
 template <bool DEV>
-__global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) {
+__global__ void __launch_bounds__(2 * kRolloutBlock) k_rollout(Params p, Buffers b) {
+    __shared__ float4 s_n[2][kRolloutBlock];   // DEV: normals of steps t (read) and t + 1 (being written)
     __shared__ float4 s_U[kMaxTStaged];   // the shifted nominal U*_t of this controller (L1-latency reads)
     const int bb = blockIdx.y;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lt = threadIdx.x % kRolloutBlock;
+    const int k = blockIdx.x * kRolloutBlock + lt;
     const unsigned long long step = *b.step;
     const int sh = step > 0 ? 1 : 0;
     for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
@@ -119,7 +149,12 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
         if (blockIdx.x == 0) reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] = u;
     }
     __syncthreads();
-    if (k >= p.K) return;
+    if (DEV && threadIdx.x >= kRolloutBlock) {
+        rollout_noise_producer(p, b, bb, lt, k, step, s_n);
+        return;
+    }
+    const bool valid = k < p.K;   // DEV: threads past K still meet every barrier (no stores)
+    if (!DEV && !valid) return;
     const float* x0 = b.x0 + bb * 10;
     float x[10];
 #pragma unroll
@@ -137,15 +172,15 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity, inv_mass = 1.f / p.mass;
     float part = 0.f;
     // software pipelining: the noise / nominal of step t+1 are produced while step t integrates
-    float4 n_next = DEV ? philox_normals(gidx, 0, step, p.seed) : b.noise[col];
+    float4 n_next = DEV ? make_float4(0.f, 0.f, 0.f, 0.f) : b.noise[col];
+    if (DEV) named_sync_rollout();   // slot 0 written
     auto nominal = [&](int t) { return t < kMaxTStaged ? s_U[t] : Uo[min(t + sh, p.T - 1)]; };
     float4 U_next = nominal(0);
     for (int t = 0; t < p.T; ++t) {
-        const float4 n = n_next;
+        const float4 n = DEV ? s_n[t & 1][lt] : n_next;
         const float4 U = U_next;
-        if (DEV) b.noise[(long long)t * NK + col] = n;   // for k_softmin (and the debug copy)
         if (t + 1 < p.T) {
-            n_next = DEV ? philox_normals(gidx, t + 1, step, p.seed) : b.noise[(long long)(t + 1) * NK + col];
+            if (!DEV) n_next = b.noise[(long long)(t + 1) * NK + col];
             U_next = nominal(t + 1);
         }
         const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
@@ -178,7 +213,8 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
         }
         const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
         const long long s = ((long long)bb * p.T + t) * p.K + k;
-        if (p.rps == 2) {
+        if (!valid) {
+        } else if (p.rps == 2) {
             const float sc = nv >= 1e-6f ? __fdividef(p.fd_h, nv) : 0.f;
             b.rows[2 * s] = make_float4(pc[0], pc[1], pc[2], nv);
             b.rows[2 * s + 1] = make_float4(pc[0] + sc * dv[0], pc[1] + sc * dv[1], pc[2] + sc * dv[2], 0.f);
@@ -187,8 +223,9 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout(Params p, Buffers b) 
         }
         const float dx = x[0] - gc[0], dy = x[1] - gc[1], dz = x[2] - gc[2];
         part += p.w_goal * (dx * dx + dy * dy + dz * dz) + p.w_u * (u0 * u0 + u1 * u1 + u2 * u2 + u3 * u3);
+        if (DEV) named_sync_rollout();   // slot t & 1 consumed; slot (t + 1) & 1 written
     }
-    b.partial[col] = part;
+    if (valid) b.partial[col] = part;
 }
 
 // ------------------------------------------------------------------ K1 (paper model): rotor rollout
@@ -222,10 +259,12 @@ __device__ __forceinline__ void dyn_rotor(const Params& p, const float* x, const
 // step to x_{k+1} (then q renormalised, w and T clamped; reading P4) and the progress term
 // |p_{k+1} - g|^2 - |p_k - g|^2. The SDF hinge term q_sdf max(0, d_safe - s) is added by the MLP kernel.
 template <bool DEV>
-__global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffers b) {
+__global__ void __launch_bounds__(2 * kRolloutBlock) k_rollout_paper(Params p, Buffers b) {
+    __shared__ float4 s_n[2][kRolloutBlock];   // DEV: normals of steps t (read) and t + 1 (being written)
     __shared__ float4 s_U[kMaxTStaged];
     const int bb = blockIdx.y;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lt = threadIdx.x % kRolloutBlock;
+    const int k = blockIdx.x * kRolloutBlock + lt;
     const unsigned long long step = *b.step;
     const int sh = step > 0 ? 1 : 0;
     for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
@@ -234,7 +273,12 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffe
         if (blockIdx.x == 0) reinterpret_cast<float4*>(b.U_nom)[(long long)bb * p.T + t] = u;
     }
     __syncthreads();
-    if (k >= p.K) return;
+    if (DEV && threadIdx.x >= kRolloutBlock) {
+        rollout_noise_producer(p, b, bb, lt, k, step, s_n);
+        return;
+    }
+    const bool valid = k < p.K;   // DEV: threads past K still meet every barrier (no stores)
+    if (!DEV && !valid) return;
     float x[17];
 #pragma unroll
     for (int i = 0; i < 17; ++i) x[i] = __ldg(b.x0 + bb * 17 + i);
@@ -251,14 +295,14 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffe
     const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f;
     float part = 0.f;
-    float4 n_next = DEV ? philox_normals(gidx, 0, step, p.seed) : b.noise[col];
+    float4 n_next = DEV ? make_float4(0.f, 0.f, 0.f, 0.f) : b.noise[col];
+    if (DEV) named_sync_rollout();   // slot 0 written
     float4 U_next = nominal(0);
     for (int t = 0; t < p.T; ++t) {
-        const float4 n = n_next;
+        const float4 n = DEV ? s_n[t & 1][lt] : n_next;
         const float4 U = U_next;
-        if (DEV) b.noise[(long long)t * NK + col] = n;
         if (t + 1 < p.T) {
-            n_next = DEV ? philox_normals(gidx, t + 1, step, p.seed) : b.noise[(long long)(t + 1) * NK + col];
+            if (!DEV) n_next = b.noise[(long long)(t + 1) * NK + col];
             U_next = nominal(t + 1);
         }
         float u[4];
@@ -271,7 +315,7 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffe
 #pragma unroll
         for (int r = 0; r < 3; ++r) pc[r] = R[3 * r] * x[0] + R[3 * r + 1] * x[1] + R[3 * r + 2] * x[2] + tq[r];
         const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
-        b.rows[((long long)bb * p.T + t) * p.K + k] = make_float4(pc[0], pc[1], pc[2], nv);
+        if (valid) b.rows[((long long)bb * p.T + t) * p.K + k] = make_float4(pc[0], pc[1], pc[2], nv);
         // cos(psi - psi_gate) as the dot of unit heading and line-of-sight vectors (atan2(0,0) = 0 -> (1,0))
         const float hx = 1.f - 2.f * (x[8] * x[8] + x[9] * x[9]), hy = 2.f * (x[6] * x[9] + x[7] * x[8]);
         const float lx = gc[0] - x[0], ly = gc[1] - x[1];
@@ -303,18 +347,19 @@ __global__ void __launch_bounds__(kRolloutBlock) k_rollout_paper(Params p, Buffe
         for (int i = 13; i < 17; ++i) x[i] = clampf(x[i], 0.f, p.thrust_max);
         const float d1 = (x[0] - gc[0]) * (x[0] - gc[0]) + (x[1] - gc[1]) * (x[1] - gc[1]) + (x[2] - gc[2]) * (x[2] - gc[2]);
         part += p.q_gate * (d1 - d0) + p.q_vis * vis;
+        if (DEV) named_sync_rollout();
     }
-    b.partial[col] = part;
+    if (valid) b.partial[col] = part;
 }
 
 void launch_rollout(const Params& p, const Buffers& b, bool device_noise, cudaStream_t s) {
     dim3 grid((p.K + kRolloutBlock - 1) / kRolloutBlock, p.n_ctrl);
     if (p.model == MPPI_MODEL_PAPER) {
-        if (device_noise) k_rollout_paper<true><<<grid, kRolloutBlock, 0, s>>>(p, b);
+        if (device_noise) k_rollout_paper<true><<<grid, 2 * kRolloutBlock, 0, s>>>(p, b);
         else k_rollout_paper<false><<<grid, kRolloutBlock, 0, s>>>(p, b);
         return;
     }
-    if (device_noise) k_rollout<true><<<grid, kRolloutBlock, 0, s>>>(p, b);
+    if (device_noise) k_rollout<true><<<grid, 2 * kRolloutBlock, 0, s>>>(p, b);   // + noise producer warps
     else k_rollout<false><<<grid, kRolloutBlock, 0, s>>>(p, b);
 }
 
