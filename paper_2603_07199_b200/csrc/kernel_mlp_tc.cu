@@ -242,6 +242,16 @@ __device__ __forceinline__ float tanh_approx(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Two IEEE fp32 FMAs in one FFMA2 instruction (sm_100): lane-wise a * b + c, bitwise equal to fmaf.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
 // Biases (and, for layer 1, the position weights and folded bias) are stored pre-scaled by
 // kPre<ACT> so that SiLU needs one FFMA to form h = x/2: silu(x) = x sigmoid(x) = h + h tanh(h).
 template <int ACT>
@@ -266,6 +276,10 @@ __device__ __forceinline__ uint32_t act_pack(float x0, float x1) {
         uint32_t r;
         asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x1), "f"(x0));
         return r;
+    } else if constexpr (ACT == MPPI_ACT_SILU) {   // h + h tanh(h) for both halves in one FFMA2
+        const float2 h = make_float2(x0, x1);
+        const float2 s = ffma2(h, make_float2(tanh_approx(x0), tanh_approx(x1)), h);
+        return pack_bf16x2(s.x, s.y);
     } else {
         return pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
     }
@@ -476,15 +490,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
             if (tracer) TC_TRACE(trole, 11, 0, 0, sl, t1);
             const float4 q = row_of(i);
+            const float2 qx2 = make_float2(q.x, q.x), qy2 = make_float2(q.y, q.y), qz2 = make_float2(q.z, q.z);
             issue_rows(i + C::NSLOT);   // that buffer was last read by tile i - NSLOT (this group, behind its bar)
             const long long row0 = tile_row0(t1);
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             if (lo != staged) {   // uniform across the group
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);   // nobody in the group still reads the old staging
-                for (int j = gtid; j < H; j += gthreads) {
-                    const float4 w = w1p[j];
-                    const float bv = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] : 0.f;
-                    w1g[j] = make_float4(w.x * kP, w.y * kP, w.z * kP, bv * kP);
+                // pair-major for FFMA2: [j/2] -> (w0x, w1x, w0y, w1y), (w0z, w1z, b0, b1), scaled by kP
+                for (int jp = gtid; jp < H / 2; jp += gthreads) {
+                    const float4 w0 = w1p[2 * jp], w1 = w1p[2 * jp + 1];
+                    const float b0 = lo < p.n_ctrl ? b1f[(size_t)lo * H + 2 * jp] : 0.f;
+                    const float b1 = lo < p.n_ctrl ? b1f[(size_t)lo * H + 2 * jp + 1] : 0.f;
+                    w1g[2 * jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
+                    w1g[2 * jp + 1] = make_float4(w0.z * kP, w1.z * kP, b0 * kP, b1 * kP);
                 }
                 staged = lo;
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);
@@ -503,20 +521,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!any_far) {
 #pragma unroll
                         for (int i2 = 0; i2 < kCW; i2 += 2) {
-                            const float4 w0 = w1g[j0 + i2], w1 = w1g[j0 + i2 + 1];
-                            const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, w0.w)));
-                            const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, w1.w)));
-                            packed[i2 / 2] = act_pack<ACT>(x0, x1);
+                            const float4 wa = w1g[j0 + i2], wb = w1g[j0 + i2 + 1];   // pair (j0+i2, j0+i2+1)
+                            const float2 x = ffma2(make_float2(wa.x, wa.y), qx2,
+                                                   ffma2(make_float2(wa.z, wa.w), qy2,
+                                                         ffma2(make_float2(wb.x, wb.y), qz2, make_float2(wb.z, wb.w))));
+                            packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     } else {   // rare: the tile crosses a controller boundary
 #pragma unroll
                         for (int i2 = 0; i2 < kCW; i2 += 2) {
-                            const float4 w0 = w1g[j0 + i2], w1 = w1g[j0 + i2 + 1];
-                            const float b0 = bfar ? __ldg(bfar + j0 + i2) * kP : w0.w;
-                            const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : w1.w;
-                            const float x0 = fmaf(w0.x, q.x, fmaf(w0.y, q.y, fmaf(w0.z, q.z, b0)));
-                            const float x1 = fmaf(w1.x, q.x, fmaf(w1.y, q.y, fmaf(w1.z, q.z, b1)));
-                            packed[i2 / 2] = act_pack<ACT>(x0, x1);
+                            const float4 wa = w1g[j0 + i2], wb = w1g[j0 + i2 + 1];
+                            const float b0 = bfar ? __ldg(bfar + j0 + i2) * kP : wb.z;
+                            const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : wb.w;
+                            const float2 x = ffma2(make_float2(wa.x, wa.y), qx2,
+                                                   ffma2(make_float2(wa.z, wa.w), qy2,
+                                                         ffma2(make_float2(wb.x, wb.y), qz2, make_float2(b0, b1))));
+                            packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     }
                     tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
@@ -534,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (sl < n_my) layer1(sl);
         for (long long i = sl; i < n_my; i += C::NSLOT) {
             uint32_t keep[C::NH > 1 ? C::QW / 2 : 1];   // unit-0 activations (bf16x2) until unit 1 is done
-            float sdot = 0.f;
+            float2 sdot2 = make_float2(0.f, 0.f);
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
@@ -564,12 +584,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
                                 const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
-                                const float x0 = fmaf(__uint_as_float(acc[i2]), kP, bv.x);
-                                const float x1 = fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y);
-                                const float x2 = fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z);
-                                const float x3 = fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w);
-                                packed[i2 / 2] = act_pack<ACT>(x0, x1);
-                                packed[i2 / 2 + 1] = act_pack<ACT>(x2, x3);
+                                const float2 x01 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
+                                                         make_float2(kP, kP), make_float2(bv.x, bv.y));
+                                const float2 x23 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
+                                                         make_float2(kP, kP), make_float2(bv.z, bv.w));
+                                packed[i2 / 2] = act_pack<ACT>(x01.x, x01.y);
+                                packed[i2 / 2 + 1] = act_pack<ACT>(x23.x, x23.y);
                             }
                             if (h < C::NH - 1) {
 #pragma unroll
@@ -585,14 +605,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
                                 const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
                                 const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i2);
-                                const uint32_t p0 = act_pack<ACT>(fmaf(__uint_as_float(acc[i2]), kP, bv.x),
-                                                                  fmaf(__uint_as_float(acc[i2 + 1]), kP, bv.y));
-                                const uint32_t p1 = act_pack<ACT>(fmaf(__uint_as_float(acc[i2 + 2]), kP, bv.z),
-                                                                  fmaf(__uint_as_float(acc[i2 + 3]), kP, bv.w));
-                                sdot = fmaf(__uint_as_float(p0 << 16), wv.x, sdot);
-                                sdot = fmaf(__uint_as_float(p0 & 0xFFFF0000u), wv.y, sdot);
-                                sdot = fmaf(__uint_as_float(p1 << 16), wv.z, sdot);
-                                sdot = fmaf(__uint_as_float(p1 & 0xFFFF0000u), wv.w, sdot);
+                                const float2 x01 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
+                                                         make_float2(kP, kP), make_float2(bv.x, bv.y));
+                                const float2 x23 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
+                                                         make_float2(kP, kP), make_float2(bv.z, bv.w));
+                                const uint32_t p0 = act_pack<ACT>(x01.x, x01.y);
+                                const uint32_t p1 = act_pack<ACT>(x23.x, x23.y);
+                                // output dot in two interleaved partial sums (even / odd neurons)
+                                sdot2 = ffma2(make_float2(__uint_as_float(p0 << 16), __uint_as_float(p0 & 0xFFFF0000u)),
+                                              make_float2(wv.x, wv.y), sdot2);
+                                sdot2 = ffma2(make_float2(__uint_as_float(p1 << 16), __uint_as_float(p1 & 0xFFFF0000u)),
+                                              make_float2(wv.z, wv.w), sdot2);
                             }
                         }
                     }
@@ -607,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // ---- output of this tile: combine column groups, FD pair, write
             const long long tile = tile_of(i);
-            part[cgi * kTileRows + row_in_tile] = sdot;
+            part[cgi * kTileRows + row_in_tile] = sdot2.x + sdot2.y;
             named_bar_sync(1 + sl, gthreads);
             if (cgi == 0) {
                 float sv = __ldg(b_out);
