@@ -179,6 +179,24 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
             : "memory");
     }
 }
+// D[tmem] (+)= A[smem] x B[smem]^T
+template <int CG>
+__device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -227,6 +245,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("ba
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// UMMA shared-memory descriptor: K-major, no swizzle (8-row x 16-byte core matrices), K = 16 operand:
+// the two K cores of a row group 128 B apart (LBO), 8-row groups 256 B apart (SBO).
+__device__ __forceinline__ uint64_t smem_desc_kmajor_noswz(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+           ((uint64_t)1 << 46);
 }
 // Instruction descriptor kind::f16: D fp32, A/B bf16, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
@@ -308,10 +332,19 @@ struct Cfg {
     static constexpr int MMA_M = 128 * CG;
     static_assert(A_OFF + H / 2 <= SLOT_COLS && QW % kCW == 0 && RB % 8 == 0, "TMEM / unit layout");
     // smem carve-up (offsets from the 1024-aligned base)
-    static constexpr int OFF_HB = W_BYTES;                           // [G][H] fp32 biases
-    static constexpr int OFF_WO = OFF_HB + 4 * G * H;                // [H] output weights
-    static constexpr int OFF_W1 = OFF_WO + 4 * H;                    // [NSLOT groups][H] float4 (W1p, b1'), scaled
-    static constexpr int OFF_PART = OFF_W1 + NSLOT * 16 * H;         // [NSLOT][COLG][128] partial dots
+    // hidden-layer biases enter the accumulator through one extra K = 16 MMA per unit: A = a constant
+    // "ones" tile [128 rows][1, 1, 0 x 14], B = [b_hi, b_lo, 0 x 14] per output row (bf16 split of the
+    // kP-scaled fp32 bias), both no-swizzle K-major -- so the epilogue adds nothing
+    static constexpr int BIAS_UNIT = RB * 32;                        // RB rows x 16 bf16
+    static constexpr int BIAS_BYTES = G * NH * BIAS_UNIT;
+    static constexpr int IMG_BYTES = W_BYTES + BIAS_BYTES;           // weight image per CTA (rank)
+    static constexpr int OFF_BIAS = W_BYTES;
+    static constexpr int OFF_ONES = OFF_BIAS + BIAS_BYTES;           // [128 rows][16] bf16 ones tile
+    static constexpr int OFF_WO = OFF_ONES + kTileRows * 32;         // [H] output weights
+    static constexpr int OFF_W1XY = OFF_WO + 4 * H;                  // [H/2] (w0x, w1x, w0y, w1y) layer-1 positions, scaled
+    static constexpr int OFF_W1Z = OFF_W1XY + 8 * H;                 // [H/2] (w0z, w1z)
+    static constexpr int OFF_B1 = OFF_W1Z + 4 * H;                   // [NSLOT groups][H] folded bias b1', scaled
+    static constexpr int OFF_PART = OFF_B1 + NSLOT * 4 * H;          // [NSLOT][COLG][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
     static constexpr int OFF_BAR = OFF_ROWS + NROWBUF * 16 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
@@ -335,9 +368,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t raw_u32 = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024u - (raw_u32 & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
-    float* s_hb = reinterpret_cast<float*>(smem + C::OFF_HB);
+    float4* s_w1xy = reinterpret_cast<float4*>(smem + C::OFF_W1XY);
+    float2* s_w1z = reinterpret_cast<float2*>(smem + C::OFF_W1Z);
     float* s_wo = reinterpret_cast<float*>(smem + C::OFF_WO);
-    float4* s_w1 = reinterpret_cast<float4*>(smem + C::OFF_W1);
+    float* s_b1 = reinterpret_cast<float*>(smem + C::OFF_B1);
     float* s_part = reinterpret_cast<float*>(smem + C::OFF_PART);
     const uint32_t bar0 = sbase + C::OFF_BAR;
     auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
@@ -353,7 +387,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
 
     // ---- setup
-    for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
+    for (int jp = threadIdx.x; jp < H / 2; jp += kThreads) {
+        const float4 w0 = w1p[2 * jp], w1 = w1p[2 * jp + 1];
+        s_w1xy[jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
+        s_w1z[jp] = make_float2(w0.z * kP, w1.z * kP);
+    }
+    for (int r = threadIdx.x; r < kTileRows; r += kThreads) {   // ones tile: row r = [1, 1, 0 x 14] (bf16)
+        uint32_t* o = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (r / 8) * 256 + (r % 8) * 16);
+        o[0] = 0x3F803F80u;
+        o[1] = o[2] = o[3] = 0u;
+        o[32] = o[33] = o[34] = o[35] = 0u;   // K core 1 (128 B further)
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA operand reads
     for (int i = threadIdx.x; i < H; i += kThreads) s_wo[i] = w_out[i];
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NSLOT; ++i) {
@@ -391,11 +436,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 1) {
         // ================= weight loader: this CTA's share of every unit, once
         if (lane == 0 && group < n_tiles) {
-            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)C::W_BYTES);
-            const uint8_t* src = wimg + (size_t)rank * C::W_BYTES;
+            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)C::IMG_BYTES);
+            const uint8_t* src = wimg + (size_t)rank * C::IMG_BYTES;
             for (int u = 0; u < G * C::NH; ++u)
                 bulk_g2s(sbase + (uint32_t)(u * C::UNIT_BYTES), src + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
                          bar(BAR_WLOCAL));
+            bulk_g2s(sbase + (uint32_t)C::OFF_BIAS, src + C::W_BYTES, C::BIAS_BYTES, bar(BAR_WLOCAL));
             mbar_wait(bar(BAR_WLOCAL), 0);
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
             else mbar_arrive_local(bar(BAR_WREADY));
@@ -424,11 +470,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
                             const uint32_t a_t = d_t + (uint32_t)C::A_OFF;
                             const uint32_t b_unit = sbase + (uint32_t)((l * C::NH + h) * C::UNIT_BYTES);
+                            // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
+                            tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
+                                          smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
+                                          idesc, 0u);
 #pragma unroll
                             for (int j = 0; j < H / 16; ++j) {
                                 const int kk = j * 16;
                                 const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
-                                tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, j > 0 ? 1u : 0u);
+                                tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
                             }
                             tc_commit<CG>(bar(BAR_MMA + sl));
                             TC_TRACE(0, 2, l, h, sl, i0);
@@ -454,8 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int trole = 1 + sl;
         const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
         uint32_t mma_cnt = 0;
-        long long staged = -1;                     // controller whose (W1p, b1') sits in this group's s_w1
-        float4* w1g = s_w1 + sl * H;
+        long long staged = -1;                     // controller whose b1' sits in this group's b1g
+        float* b1g = s_b1 + sl * H;
         float* part = s_part + sl * kColGroups * kTileRows;
         auto arrive_sched = [&](int i) {           // epilogue -> MMA issuer (leader CTA)
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(i));
@@ -496,14 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             if (lo != staged) {   // uniform across the group
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);   // nobody in the group still reads the old staging
-                // pair-major for FFMA2: [j/2] -> (w0x, w1x, w0y, w1y), (w0z, w1z, b0, b1), scaled by kP
-                for (int jp = gtid; jp < H / 2; jp += gthreads) {
-                    const float4 w0 = w1p[2 * jp], w1 = w1p[2 * jp + 1];
-                    const float b0 = lo < p.n_ctrl ? b1f[(size_t)lo * H + 2 * jp] : 0.f;
-                    const float b1 = lo < p.n_ctrl ? b1f[(size_t)lo * H + 2 * jp + 1] : 0.f;
-                    w1g[2 * jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
-                    w1g[2 * jp + 1] = make_float4(w0.z * kP, w1.z * kP, b0 * kP, b1 * kP);
-                }
+                for (int j = gtid; j < H; j += gthreads) b1g[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
                 staged = lo;
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);
             }
@@ -521,21 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!any_far) {
 #pragma unroll
                         for (int i2 = 0; i2 < kCW; i2 += 2) {
-                            const float4 wa = w1g[j0 + i2], wb = w1g[j0 + i2 + 1];   // pair (j0+i2, j0+i2+1)
+                            const int jp = (j0 + i2) / 2;   // neuron pair (j0+i2, j0+i2+1)
+                            const float4 wa = s_w1xy[jp];
                             const float2 x = ffma2(make_float2(wa.x, wa.y), qx2,
                                                    ffma2(make_float2(wa.z, wa.w), qy2,
-                                                         ffma2(make_float2(wb.x, wb.y), qz2, make_float2(wb.z, wb.w))));
+                                                         ffma2(s_w1z[jp], qz2, *reinterpret_cast<const float2*>(b1g + j0 + i2))));
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     } else {   // rare: the tile crosses a controller boundary
 #pragma unroll
                         for (int i2 = 0; i2 < kCW; i2 += 2) {
-                            const float4 wa = w1g[j0 + i2], wb = w1g[j0 + i2 + 1];
-                            const float b0 = bfar ? __ldg(bfar + j0 + i2) * kP : wb.z;
-                            const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : wb.w;
+                            const int jp = (j0 + i2) / 2;
+                            const float4 wa = s_w1xy[jp];
+                            const float b0 = bfar ? __ldg(bfar + j0 + i2) * kP : b1g[j0 + i2];
+                            const float b1 = bfar ? __ldg(bfar + j0 + i2 + 1) * kP : b1g[j0 + i2 + 1];
                             const float2 x = ffma2(make_float2(wa.x, wa.y), qx2,
-                                                   ffma2(make_float2(wa.z, wa.w), qy2,
-                                                         ffma2(make_float2(wb.x, wb.y), qz2, make_float2(b0, b1))));
+                                                   ffma2(make_float2(wa.z, wa.w), qy2, ffma2(s_w1z[jp], qz2, make_float2(b0, b1))));
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     }
@@ -558,7 +602,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int l = 0; l < G; ++l) {
                 const bool last = (l == G - 1);
-                const float* hb = s_hb + l * H;
 #pragma unroll
                 for (int h = 0; h < C::NH; ++h) {
                     if (tracer) TC_TRACE(trole, 3, l, h, sl, i);
@@ -583,13 +626,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t packed[kCW / 2];
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
-                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
-                                const float2 x01 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
-                                                         make_float2(kP, kP), make_float2(bv.x, bv.y));
-                                const float2 x23 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
-                                                         make_float2(kP, kP), make_float2(bv.z, bv.w));
-                                packed[i2 / 2] = act_pack<ACT>(x01.x, x01.y);
-                                packed[i2 / 2 + 1] = act_pack<ACT>(x23.x, x23.y);
+                                // D = kP (W a + b): bias and pre-scale are already in the accumulator
+                                packed[i2 / 2] = act_pack<ACT>(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]));
+                                packed[i2 / 2 + 1] = act_pack<ACT>(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3]));
                             }
                             if (h < C::NH - 1) {
 #pragma unroll
@@ -603,14 +642,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else {
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
-                                const float4 bv = *reinterpret_cast<const float4*>(hb + j0 + i2);
                                 const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i2);
-                                const float2 x01 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
-                                                         make_float2(kP, kP), make_float2(bv.x, bv.y));
-                                const float2 x23 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
-                                                         make_float2(kP, kP), make_float2(bv.z, bv.w));
-                                const uint32_t p0 = act_pack<ACT>(x01.x, x01.y);
-                                const uint32_t p1 = act_pack<ACT>(x23.x, x23.y);
+                                const uint32_t p0 = act_pack<ACT>(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]));
+                                const uint32_t p1 = act_pack<ACT>(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3]));
                                 // output dot in two interleaved partial sums (even / odd neurons)
                                 sdot2 = ffma2(make_float2(__uint_as_float(p0 << 16), __uint_as_float(p0 & 0xFFFF0000u)),
                                               make_float2(wv.x, wv.y), sdot2);
@@ -738,33 +772,54 @@ bool mlp_tc_supported(int H, int G, int act) {
     return (H == 128 || H == 256) && G >= 1 && G <= 3 && act >= 0 && act <= 2;
 }
 
-size_t mlp_tc_weight_bytes(int H, int G) { return (size_t)G * H * H * 2; }
+size_t mlp_tc_weight_bytes(int H, int G) { return (size_t)G * H * H * 2 + (size_t)G * H * 32; }
 
-// Global image = the shared-memory images of the CTA(s) of one MMA group, [rank][layer][unit q] blocks
-// of RB x H bf16 (rank r holds rows [q UN + r RB, +RB) of W_l, UN = H/NH, RB = UN/CG); inside a block,
-// [64-wide K chunk][row n][128 B] with the 16-byte groups of row n XOR-swizzled by (n % 8) (UMMA
-// SWIZZLE_128B, K-major, 8-row atoms of 1024 B).
-void mlp_tc_pack_weights(int H, int G, const float* W, uint8_t* out) {
-    const int CG = H == 256 ? 2 : 1, NU = H == 256 ? tc::Cfg<256, 1>::NH : tc::Cfg<128, 1>::NH;
-    const int UN = H / NU, RB = UN / CG;
-    const size_t unit = (size_t)RB * H * 2;
-    const size_t per_rank = (size_t)G * NU * unit;
+// Global image = the shared-memory images of the CTA(s) of one MMA group, per rank r:
+//  * hidden layers: [layer][unit q] blocks of RB x H bf16 (rank r holds rows [q UN + r RB, +RB) of W_l,
+//    UN = 128, RB = UN/CG), scaled by kPre<act> (exact: a power of two); inside a block, [64-wide K chunk]
+//    [row n][128 B] with the 16-byte groups of row n XOR-swizzled by (n % 8) (UMMA SWIZZLE_128B, K-major);
+//  * hidden biases: [layer][unit q] blocks of RB rows x 16 bf16, row n = [b_hi, b_lo, 0 x 14] with
+//    b_hi + b_lo = kPre b (bf16 split of the fp32 value), no swizzle: [n / 8][K core][n % 8][8 bf16].
+void mlp_tc_pack_weights(int H, int G, int act, const float* W, const float* hb, uint8_t* out) {
+    const int CG = H == 256 ? 2 : 1, NH = H / 128;
+    const int UN = H / NH, RB = UN / CG;
+    const float kp = act == MPPI_ACT_SILU ? 0.5f : 1.0f;
+    const size_t unit = (size_t)RB * H * 2, bunit = (size_t)RB * 32;
+    const size_t hidden = (size_t)G * NH * unit;
+    const size_t per_rank = hidden + (size_t)G * NH * bunit;
+    auto bits_of = [](float v) {
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        return (uint16_t)(u >> 16);
+    };
+    auto bf16_rne = [](float v) {
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+        float r;
+        std::memcpy(&r, &u, 4);
+        return r;
+    };
+    std::memset(out, 0, per_rank * CG);
     for (int r = 0; r < CG; ++r)
         for (int l = 0; l < G; ++l)
-            for (int q = 0; q < NU; ++q) {
-                uint8_t* blk = out + (size_t)r * per_rank + (size_t)(l * NU + q) * unit;
-                for (int nn = 0; nn < RB; ++nn)
+            for (int q = 0; q < NH; ++q) {
+                uint8_t* blk = out + (size_t)r * per_rank + (size_t)(l * NH + q) * unit;
+                uint8_t* bblk = out + (size_t)r * per_rank + hidden + (size_t)(l * NH + q) * bunit;
+                for (int nn = 0; nn < RB; ++nn) {
+                    const int n = q * UN + r * RB + nn;
                     for (int k = 0; k < H; ++k) {
-                        const int n = q * UN + r * RB + nn;
-                        const float v = W[(size_t)l * H * H + (size_t)n * H + k];
-                        uint32_t u;
-                        std::memcpy(&u, &v, 4);   // already a bf16 value: the top 16 bits are exact
-                        const uint16_t bits = (uint16_t)(u >> 16);
+                        const uint16_t b = bits_of(W[(size_t)l * H * H + (size_t)n * H + k] * kp);   // bf16 value
                         const int kc = k / 64, w = k % 64;
                         const size_t off = (size_t)kc * RB * 128 + (size_t)nn * 128 +
                                            (size_t)(((w / 8) ^ (nn % 8)) * 16) + (size_t)(w % 8) * 2;
-                        std::memcpy(blk + off, &bits, 2);
+                        std::memcpy(blk + off, &b, 2);
                     }
+                    const float bv = hb[(size_t)l * H + n] * kp;
+                    const float hi = bf16_rne(bv), lo = bf16_rne(bv - hi);
+                    const uint16_t pair[2] = {bits_of(hi), bits_of(lo)};
+                    std::memcpy(bblk + (size_t)(nn / 8) * 256 + (size_t)(nn % 8) * 16, pair, 4);
+                }
             }
 }
 

@@ -385,7 +385,7 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     if (G > 0) {
         if (bf) {
             std::vector<uint8_t> img(mlp_tc_weight_bytes(H, G));
-            mlp_tc_pack_weights(H, G, hw.data(), img.data());
+            mlp_tc_pack_weights(H, G, c.activation, hw.data(), hb.data(), img.data());
             CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_wbf, img.data(), img.size(), cudaMemcpyHostToDevice));
         } else {
             CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_w32, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice));

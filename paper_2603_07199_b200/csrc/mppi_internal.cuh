@@ -75,7 +75,8 @@ int mlp_tc_trace_copy(unsigned long long* host, int max_entries);   // debug bui
 size_t mlp_tc_weight_bytes(int H, int n_gemm);
 // Lay out bf16 weights of the n_gemm hidden layers (host, [l][H][H] fp32 nn.Linear order, already
 // bf16-representable) in the swizzled UMMA image the kernel copies to shared memory.
-void mlp_tc_pack_weights(int H, int n_gemm, const float* W, uint8_t* out);
+// The hidden biases hb [n_gemm][H] go into the same image (added by the tensor cores).
+void mlp_tc_pack_weights(int H, int n_gemm, int act, const float* W, const float* hb, uint8_t* out);
 // rows_mode: rows are per-state query rows of the step (writes per-state SDF terms) when states_mode,
 // else arbitrary rows for mppi_sdf_eval (writes s per row only).
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
