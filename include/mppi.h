@@ -66,6 +66,11 @@ enum { MPPI_NOISE_DEVICE = 0, MPPI_NOISE_EXTERNAL = 1 };
  *       + q_sdf max(0, d_safe - s(p_k))                      (Eqs. 6-10),
  *   so the SDF is queried at x_0..x_{T-1}; w_goal, w_sdf, sdf_scale, w_u are unused and w_guide must be 0. */
 enum { MPPI_MODEL_BASELINE = 0, MPPI_MODEL_PAPER = 1 };
+/* SDF provider. MPPI_SDF_MLP: the neural Gate-SDF g_phi(z, p_c) (weights + latents).
+ * MPPI_SDF_GATE: the analytic Gate-SDF of Eq. 2, s = gate_c + |x| gate_tana - max(|y|, |z|)
+ * with p_c = (x, y, z) in the query frame, which must then be the gate frame (gate plane x = 0); no
+ * weights are needed and mppi_set_latent only sets T_q (z is ignored). */
+enum { MPPI_SDF_MLP = 0, MPPI_SDF_GATE = 1 };
 
 typedef struct {
     int32_t abi_version;       /* MPPI_ABI_VERSION                                                 */
@@ -92,6 +97,8 @@ typedef struct {
     float inertia[3];                           /* MPPI_MODEL_PAPER: diag(J) (kg m^2)               */
     float thrust_max, rate_max;                 /* MPPI_MODEL_PAPER: rotor thrust (N), body-rate (rad/s) limits */
     float q_gate, q_vis, q_sdf, d_safe;         /* MPPI_MODEL_PAPER: Eq. 10 weights, Eq. 8 clearance (m) */
+    int32_t sdf_provider;                       /* MPPI_SDF_*                                       */
+    float gate_c, gate_tana;                    /* MPPI_SDF_GATE: inner half-width c (m), tan(alpha) */
 } mppi_config;
 
 /* Bytes of device workspace mppi_create() needs for this config (0 if the config is invalid). */

@@ -96,8 +96,16 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def make_cfg(cfg, sdf_mode: int = 0, gate_c: float = 0.5, gate_tana: float = 0.375, **override) -> OracleCfg:
-    """Build the C struct from a synth.MPPIConfig (duck-typed)."""
+def make_cfg(cfg, sdf_mode: int | None = None, gate_c: float | None = None, gate_tana: float | None = None,
+             **override) -> OracleCfg:
+    """Build the C struct from a synth.MPPIConfig (duck-typed). sdf_mode / gate_c / gate_tana default to
+    the config's sdf_provider / gate_c / gate_tana (else the MLP, c = 0.5, tan(alpha) = 0.375)."""
+    if sdf_mode is None:
+        sdf_mode = getattr(cfg, "sdf_provider", 0)
+    if gate_c is None:
+        gate_c = getattr(cfg, "gate_c", 0.5)
+    if gate_tana is None:
+        gate_tana = getattr(cfg, "gate_tana", 0.375) if getattr(cfg, "sdf_provider", 0) == 1 else 0.375
     oc = OracleCfg()
     oc.n_ctrl, oc.K, oc.T = cfg.n_ctrl, cfg.K, cfg.T
     oc.dt, oc.lam, oc.mass, oc.gravity = cfg.dt, cfg.lam, cfg.mass, cfg.gravity

@@ -651,6 +651,41 @@ void launch_combine(const Params& p, const Buffers& b, const float* recs, int R,
     k_combine<<<(n + 127) / 128, 128, 0, s>>>(p, b, recs, R);
 }
 
+// ------------------------------------------------------------------ analytic Gate-SDF provider (F4)
+// s_guide(p) = c + |x| tan(alpha) - max(|y|, |z|) in the gate frame (Eqs. 1-2), on the
+// step's query rows; writes the same SDF stage term the MLP epilogue would (model 0: 50 e^{-s/0.1} and the
+// forward-difference guidance; model 1: the Eq. 8 hinge). Thread per state.
+__device__ __forceinline__ float gate_sdf(const Params& p, float4 q) {
+    return p.gate_c + fabsf(q.x) * p.gate_tana - fmaxf(fabsf(q.y), fabsf(q.z));
+}
+
+__global__ void k_sdf_gate(Params p, Buffers b, float* sdf_out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n = (long long)p.n_ctrl * p.T * p.K;
+    if (i >= n) return;
+    const float4 q0 = b.rows[i * p.rps];
+    const float s0 = gate_sdf(p, q0);
+    float s1 = s0;
+    if (p.rps == 2) s1 = gate_sdf(p, b.rows[i * 2 + 1]);
+    if (sdf_out) {
+        sdf_out[i * p.rps] = s0;
+        if (p.rps == 2) sdf_out[i * 2 + 1] = s1;
+    }
+    float term;
+    if (p.model == MPPI_MODEL_PAPER) {
+        term = p.q_sdf * fmaxf(p.d_safe - s0, 0.f);
+    } else {
+        term = p.w_sdf * expf(fminf(-s0 * p.inv_sdf_scale, p.sdf_exp_max));
+        if (p.rps == 2) term -= p.w_guide * q0.w * (s1 - s0) * p.inv_fd_h;
+    }
+    b.terms[i] = term;
+}
+
+void launch_sdf_gate(const Params& p, const Buffers& b, float* sdf_out, cudaStream_t s) {
+    const long long n = (long long)p.n_ctrl * p.T * p.K;
+    k_sdf_gate<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, b, sdf_out);
+}
+
 // ------------------------------------------------------------------ K5: latent fold
 // b1'[b][j] = sum_l W1[j][3+l] z_b[l] + b1[j]: the latent concat of PAPER.md:40 folded into a bias.
 __global__ void k_fold(Params p, Buffers b, int c0) {

@@ -157,6 +157,9 @@ static mppi_status validate(const mppi_config* c) {
     if (!(c->sdf_scale > 0.f)) return fail(MPPI_ERR_INVALID, "sdf_scale > 0");
     if (c->w_guide != 0.f && !(c->fd_h > 0.f)) return fail(MPPI_ERR_INVALID, "fd_h > 0 with guidance");
     if (c->model != MPPI_MODEL_BASELINE && c->model != MPPI_MODEL_PAPER) return fail(MPPI_ERR_INVALID, "bad model");
+    if (c->sdf_provider != MPPI_SDF_MLP && c->sdf_provider != MPPI_SDF_GATE) return fail(MPPI_ERR_INVALID, "bad sdf_provider");
+    if (c->sdf_provider == MPPI_SDF_GATE && (!std::isfinite(c->gate_c) || !(c->gate_tana >= 0.f) || !std::isfinite(c->gate_tana)))
+        return fail(MPPI_ERR_INVALID, "gate_c finite, gate_tana >= 0");
     if (c->model == MPPI_MODEL_PAPER) {
         if (c->w_guide != 0.f) return fail(MPPI_ERR_INVALID, "the paper model has no guidance term (w_guide must be 0)");
         if (!(c->inertia[0] > 0.f) || !(c->inertia[1] > 0.f) || !(c->inertia[2] > 0.f) || !(c->arm > 0.f))
@@ -277,6 +280,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.inv_Jx = 1.f / cfg->inertia[0]; p.inv_Jy = 1.f / cfg->inertia[1]; p.inv_Jz = 1.f / cfg->inertia[2];
     p.thrust_max = cfg->thrust_max; p.rate_max = cfg->rate_max;
     p.q_gate = cfg->q_gate; p.q_vis = cfg->q_vis; p.q_sdf = cfg->q_sdf; p.d_safe = cfg->d_safe;
+    p.sdf_provider = cfg->sdf_provider; p.gate_c = cfg->gate_c; p.gate_tana = cfg->gate_tana;
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
     ctx->latent_set.assign(cfg->n_ctrl, 0);
 
@@ -399,7 +403,8 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
 mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q) {
     CHECK_CTX(ctx);
     const mppi_config& c = ctx->cfg;
-    if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "set weights before latents");
+    const bool gate = c.sdf_provider == MPPI_SDF_GATE;
+    if (!ctx->weights && !gate) return fail(MPPI_ERR_NOT_READY, "set weights before latents");
     if (ctrl < -1 || ctrl >= c.n_ctrl || (!z && c.latent_dim > 0) || !T_q) return fail(MPPI_ERR_INVALID, "bad ctrl / NULL");
     const int c0 = ctrl < 0 ? 0 : ctrl, cnt = ctrl < 0 ? c.n_ctrl : 1;
     for (int i = 0; i < cnt * 12; ++i)
@@ -409,7 +414,7 @@ mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const f
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.z + (size_t)c0 * c.latent_dim, z, sizeof(float) * cnt * c.latent_dim,
                                       cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.Tq + (size_t)c0 * 12, T_q, sizeof(float) * cnt * 12, cudaMemcpyHostToDevice, s));
-    launch_fold(ctx->p, ctx->b, c0, cnt, s);
+    if (!gate) launch_fold(ctx->p, ctx->b, c0, cnt, s);   // the analytic provider uses T_q only
     CUDA_TRY(ctx, cudaGetLastError());
     CUDA_TRY(ctx, cudaStreamSynchronize(s));   // host arrays may be reused on return
     for (int i = 0; i < cnt; ++i) ctx->latent_set[c0 + i] = 1;
@@ -460,7 +465,13 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
     launch_rollout(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
     mark(2);
-    cudaError_t e = launch_mlp_states(ctx, s);
+    cudaError_t e;
+    if (ctx->cfg.sdf_provider == MPPI_SDF_GATE) {
+        launch_sdf_gate(p, ctx->b, ctx->debug_outputs ? ctx->b.sdf_rows : nullptr, s);
+        e = cudaGetLastError();
+    } else {
+        e = launch_mlp_states(ctx, s);
+    }
     if (e != cudaSuccess) return e;
     mark(3);
     if (mode == 1 || ctx->comm) {
@@ -483,7 +494,7 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
 static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step, bool device_inputs,
                             int mode) {
     CHECK_CTX(ctx);
-    if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "weights not set");
+    if (!ctx->weights && ctx->cfg.sdf_provider != MPPI_SDF_GATE) return fail(MPPI_ERR_NOT_READY, "weights not set");
     for (char v : ctx->latent_set)
         if (!v) return fail(MPPI_ERR_NOT_READY, "latent not set for every controller");
     if (!x0 || !goal) return fail(MPPI_ERR_INVALID, "NULL x0/goal");

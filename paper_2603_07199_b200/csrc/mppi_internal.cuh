@@ -23,6 +23,9 @@ struct Params {
     float arm_d, kappa;              // arm / sqrt(2) (rotor offset along each body axis), yaw moment per thrust
     float Jx, Jy, Jz, inv_Jx, inv_Jy, inv_Jz;
     float thrust_max, rate_max, q_gate, q_vis, q_sdf, d_safe;
+    // MPPI_SDF_GATE
+    int sdf_provider;
+    float gate_c, gate_tana;
 };
 
 // Device buffers of one context (all inside the workspace).
@@ -68,6 +71,8 @@ void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaSt
 int softmin_blocks(int K);
 void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s);
 void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_count, cudaStream_t s);
+// analytic Gate-SDF (Eq. 2) on the step's query rows -> SDF stage terms (replaces the MLP launch)
+void launch_sdf_gate(const Params& p, const Buffers& b, float* sdf_out, cudaStream_t s);
 
 // tcgen05 / TMEM SDF-MLP (kernel_mlp_tc.cu)
 bool mlp_tc_supported(int H, int n_gemm, int act);

