@@ -511,3 +511,9 @@ def test_gate_sdf_provider_prefers_the_opening():
                            Ug[0].astype(np.float32), np.zeros((cfg.T, 4)))
     assert r_new["J"] <= r_nom["J"] + 1e-6
     assert s_before.shape[-1] == 1
+
+
+def test_graft_entry_smoke_runs():
+    """The driver's round-end smoke() (one configs[1]-shaped iteration checked against the oracle)."""
+    import __graft_entry__
+    __graft_entry__.smoke()
