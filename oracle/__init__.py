@@ -45,6 +45,7 @@ class OracleCfg(C.Structure):
         ("model", C.c_int32), ("arm", C.c_double), ("kappa", C.c_double), ("inertia", C.c_double * 3),
         ("thrust_max", C.c_double), ("rate_max", C.c_double),
         ("q_gate", C.c_double), ("q_vis", C.c_double), ("q_sdf", C.c_double), ("d_safe", C.c_double),
+        ("pe_bands", C.c_int32),
     ]
 
 
@@ -81,6 +82,7 @@ def lib():
         _lib.oracle_shift.argtypes = [i32, i32, P(f)]
         _lib.oracle_rotor_deriv.argtypes = [P(OracleCfg), P(d), P(d), P(d)]
         _lib.oracle_rotor_step.argtypes = [P(OracleCfg), P(d), P(d), P(d)]
+        _lib.oracle_pe.argtypes = [C.c_int, P(d), P(d)]
     return _lib
 
 
@@ -117,6 +119,7 @@ def make_cfg(cfg, sdf_mode: int | None = None, gate_c: float | None = None, gate
     oc.activation, oc.mlp_bf16 = cfg.activation, int(cfg.mlp_dtype == 1)
     oc.sdf_mode, oc.gate_c, oc.gate_tana = sdf_mode, gate_c, gate_tana
     oc.model = getattr(cfg, "model", 0)
+    oc.pe_bands = getattr(cfg, "pe_bands", 0)
     if oc.model == 1:
         oc.arm, oc.kappa, oc.thrust_max, oc.rate_max = cfg.arm, cfg.kappa, cfg.thrust_max, cfg.rate_max
         for i in range(3):
@@ -171,6 +174,13 @@ def rotor_step(oc: OracleCfg, x, u):
     x, u = _f64(x), _f64(u)
     out = np.zeros(17)
     lib().oracle_rotor_step(C.byref(oc), _p(x, C.c_double), _p(u, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def pe(bands: int, p) -> np.ndarray:
+    p = _f64(p)
+    out = np.zeros(3 + 6 * bands)
+    lib().oracle_pe(bands, _p(p, C.c_double), _p(out, C.c_double))
     return out
 
 

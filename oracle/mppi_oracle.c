@@ -22,6 +22,7 @@
  *   total cost    J = sum of weighted stage costs                  PAPER.md:185 (Eq. 10), with the
  *                 BASELINE configs[0..1] terms (||p-g_c||^2, 50 exp(-s/0.1), 0.01||u||^2, -0.5 grad s.v)
  *   analytic SDF  s_guide = c + |x| tan(a) - max(|y|,|z|)          PAPER.md:64-72 (Eqs. 1-2)
+ *   PE            g_phi(z, PE(p)), PE(p) = [p, sin(2^i pi p), cos(2^i pi p)]_{i<B}  PAPER.md:121 (reading E1)
  *   paper model   (model 1; SURVEY.md §8f F1 + F2, readings P1-P7)
  *                 x = [p, v, q, w, T], u = [T1dot..T4dot]            PAPER.md:146 (§IV-A)
  *                 J_gate = sum_k |p_{k+1}-p_wp|^2 - |p_k-p_wp|^2   PAPER.md:153 (Eq. 6)
@@ -53,6 +54,7 @@ typedef struct {
     double inertia[3];           /* model 1: diag(J) (kg m^2)                                         */
     double thrust_max, rate_max; /* model 1: T_i in [0, thrust_max] (N); |w_i| <= rate_max (rad/s)    */
     double q_gate, q_vis, q_sdf, d_safe;   /* model 1: Eq. 10 weights, Eq. 8 clearance               */
+    int32_t pe_bands;            /* positional encoding PE(p) on the MLP input (reading E1) */
 } oracle_cfg;
 
 /* ------------------------------------------------------------------ Philox4x32-10 (Salmon et al.) */
@@ -215,19 +217,36 @@ static double act_fn(int a, double v) {
     }
 }
 
-/* s = g_phi(z, p): layer 1 on [p | z] (full 3+L dot, fp64, NOT folded); hidden layers; linear output.
- * W: all layers concatenated, each [out][in] row-major (nn.Linear); b likewise. */
+/* Positional encoding ("a positional encoding applied to the spatial coordinates before
+ * concatenation"; reading E1): the raw coordinates, then per band i = 0..B-1 the six values
+ * sin(2^i pi x), sin(2^i pi y), sin(2^i pi z), cos(2^i pi x), cos(2^i pi y), cos(2^i pi z). out: 3 + 6B. */
+void oracle_pe(int bands, const double* p, double* out) {
+    const double pi = 3.14159265358979323846264338327950288;
+    for (int c = 0; c < 3; ++c) out[c] = p[c];
+    for (int i = 0; i < bands; ++i)
+        for (int c = 0; c < 3; ++c) {
+            const double a = ldexp(pi * p[c], i);
+            out[3 + 6 * i + c] = sin(a);
+            out[3 + 6 * i + 3 + c] = cos(a);
+        }
+}
+
+/* s = g_phi(z, p): layer 1 on [PE(p) | z] (PE(p) = p without PE; full dot, fp64, NOT folded); hidden
+ * layers; linear output. W: all layers concatenated, each [out][in] row-major (nn.Linear); b likewise. */
 double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p) {
     const int L = cfg->latent_dim, H = cfg->hidden;
     double* a = (double*)malloc(sizeof(double) * (size_t)H);
     double* an = (double*)malloc(sizeof(double) * (size_t)H);
     const float* Wl = W;
     const float* bl = b;
-    const int in1 = 3 + L;
+    const int npe = 3 + 6 * cfg->pe_bands;
+    double feat[3 + 6 * 16];
+    oracle_pe(cfg->pe_bands, p, feat);
+    const int in1 = npe + L;
     for (int i = 0; i < H; ++i) {
         double acc = 0.0;
-        for (int j = 0; j < 3; ++j) acc += (double)Wl[(size_t)i * in1 + j] * p[j];
-        for (int j = 0; j < L; ++j) acc += (double)Wl[(size_t)i * in1 + 3 + j] * (double)z[j];
+        for (int j = 0; j < npe; ++j) acc += (double)Wl[(size_t)i * in1 + j] * feat[j];
+        for (int j = 0; j < L; ++j) acc += (double)Wl[(size_t)i * in1 + npe + j] * (double)z[j];
         acc += (double)bl[i];
         double v = act_fn(cfg->activation, acc);
         a[i] = cfg->mlp_bf16 ? bf16_round(v) : v;

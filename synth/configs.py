@@ -55,6 +55,8 @@ class MPPIConfig:
     sdf_provider: int = 0
     gate_c: float = 0.5          # inner half-width: inner diameter 1.0 m
     gate_tana: float = 0.36397023426620234   # tan(20 deg): alpha unstated; SURVEY/SPEC.md:139-141 golden values
+    # positional encoding of the query position (reading E1): 0 = none
+    pe_bands: int = 0
 
     @property
     def u_lo(self):
@@ -78,8 +80,9 @@ class MPPIConfig:
 
     @property
     def layer_dims(self):
-        """[(in, out)] for every dense layer, nn.Linear order ([out][in] weights)."""
-        dims = [(3 + self.latent_dim, self.hidden)]
+        """[(in, out)] for every dense layer, nn.Linear order ([out][in] weights). Layer 1 reads
+        [PE(p) (3 + 6 pe_bands) | z (L)]."""
+        dims = [(3 + 6 * self.pe_bands + self.latent_dim, self.hidden)]
         dims += [(self.hidden, self.hidden)] * (self.n_hidden - 1)
         dims += [(self.hidden, 1)]
         return dims
@@ -130,6 +133,9 @@ CONFIGS["c1g"] = CONFIGS["c1"].replace(name="c1g", sdf_provider=1)
 CONFIGS["c1gs"] = CONFIGS["c1s"].replace(name="c1gs", sdf_provider=1)
 CONFIGS["c4gs"] = CONFIGS["c4s"].replace(name="c4gs", sdf_provider=1)
 CONFIGS["c5gs"] = CONFIGS["c5s"].replace(name="c5gs", sdf_provider=1)
+# Positional encoding on the configs[1] MLP: 4 bands (27 position features)
+CONFIGS["c1pe"] = CONFIGS["c1"].replace(name="c1pe", pe_bands=4)
+CONFIGS["c1pes"] = CONFIGS["c1s"].replace(name="c1pes", pe_bands=4)
 
 
 def get_config(name: str, **overrides) -> MPPIConfig:
