@@ -31,11 +31,12 @@ def mlp_flops_per_row(cfg) -> int:
     """Algorithmic flops of one SDF evaluation with the latent folded:
     layer 1 is 3-wide (+bias), hidden GEMMs H x H, output H (2 flops per MAC)."""
     H, G = cfg.hidden, cfg.n_hidden - 1
-    return 2 * (3 * H + G * H * H + H)
+    npe = 3 + 6 * getattr(cfg, "pe_bands", 0)   # position features (positional encoding, SURVEY §8f F3)
+    return 2 * (npe * H + G * H * H + H)
 
 
 def workload_name(cfg, world):
-    return (f"{cfg.name}: n_ctrl={cfg.n_ctrl} K={cfg.K} T={cfg.T} dt={cfg.dt} MLP {3 + cfg.latent_dim}->"
+    return (f"{cfg.name}: n_ctrl={cfg.n_ctrl} K={cfg.K} T={cfg.T} dt={cfg.dt} MLP {3 + 6 * cfg.pe_bands + cfg.latent_dim}->"
             f"{cfg.hidden}x{cfg.n_hidden}->1 {['softplus', 'relu', 'silu'][cfg.activation]} "
             f"{['fp32', 'bf16'][cfg.mlp_dtype]}{' + FD guidance' if cfg.fd else ''}"
             f"{f', K sharded over {world} ranks' if world > 1 and cfg.name == 'c3' else ''}")

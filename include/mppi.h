@@ -99,6 +99,10 @@ typedef struct {
     float q_gate, q_vis, q_sdf, d_safe;         /* MPPI_MODEL_PAPER: Eq. 10 weights, Eq. 8 clearance (m) */
     int32_t sdf_provider;                       /* MPPI_SDF_*                                       */
     float gate_c, gate_tana;                    /* MPPI_SDF_GATE: inner half-width c (m), tan(alpha) */
+    int32_t pe_bands;                           /* positional encoding of the SDF input:
+                                                   0, or 4 (bf16 MLP with hidden 128): layer 1 reads
+                                                   [p, sin(2^i pi p), cos(2^i pi p) (i < 4) | z], i.e.
+                                                   in_dim[0] = 3 + 6 pe_bands + latent_dim (E1) */
 } mppi_config;
 
 /* Bytes of device workspace mppi_create() needs for this config (0 if the config is invalid). */

@@ -49,6 +49,7 @@ class MppiConfig(C.Structure):
         ("thrust_max", C.c_float), ("rate_max", C.c_float),
         ("q_gate", C.c_float), ("q_vis", C.c_float), ("q_sdf", C.c_float), ("d_safe", C.c_float),
         ("sdf_provider", C.c_int32), ("gate_c", C.c_float), ("gate_tana", C.c_float),
+        ("pe_bands", C.c_int32),
     ]
 
 
@@ -142,4 +143,5 @@ def make_config(cfg, *, device: int = 0, stream: int = 0, noise_mode: str = "dev
         c.q_gate, c.q_vis, c.q_sdf, c.d_safe = cfg.q_gate, cfg.q_vis, cfg.q_sdf, cfg.d_safe
     c.sdf_provider = getattr(cfg, "sdf_provider", 0)
     c.gate_c, c.gate_tana = getattr(cfg, "gate_c", 0.5), getattr(cfg, "gate_tana", 0.0)
+    c.pe_bands = getattr(cfg, "pe_bands", 0)
     return c

@@ -310,8 +310,9 @@ __device__ __forceinline__ uint32_t act_pack(float x0, float x1) {
 }
 
 // ------------------------------------------------------------------ configuration
-template <int H, int G>
+template <int H, int G, int PEB = 0>
 struct Cfg {
+    static constexpr int NPE = 3 + 6 * PEB;                  // layer-1 position features (raw p + PE bands)
     static constexpr int CG = H == 256 ? 2 : 1;              // CTAs per MMA (cta_group)
     // A TS-form MMA (A in TMEM) streams 4 KB of A per K=16 step per CTA (M = 128): below N = 128 it runs
     // at the A-read rate, not the math rate, so units are N = 128 (two per layer for H = 256, one for 128)
@@ -344,7 +345,8 @@ struct Cfg {
     static constexpr int OFF_W1XY = OFF_WO + 4 * H;                  // [H/2] (w0x, w1x, w0y, w1y) layer-1 positions, scaled
     static constexpr int OFF_W1Z = OFF_W1XY + 8 * H;                 // [H/2] (w0z, w1z)
     static constexpr int OFF_B1 = OFF_W1Z + 4 * H;                   // [NSLOT groups][H] folded bias b1', scaled
-    static constexpr int OFF_PART = OFF_B1 + NSLOT * 4 * H;          // [NSLOT][COLG][128] partial dots
+    static constexpr int OFF_PE = OFF_B1 + NSLOT * 4 * H;            // PEB > 0: [H/2][NPE] float2 PE weights, scaled
+    static constexpr int OFF_PART = OFF_PE + (PEB > 0 ? (H / 2) * NPE * 8 : 0);   // [NSLOT][COLG][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
     static constexpr int OFF_BAR = OFF_ROWS + NROWBUF * 16 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
@@ -356,13 +358,13 @@ struct Cfg {
 enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slots]*/, BAR_WLOCAL = 12,
        BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/ };
 
-template <int H, int G, int ACT>
+template <int H, int G, int ACT, int PEB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_mlp_tc(Params p, const float4* __restrict__ rows, long long n_rows, int ctrl_fixed, int states_mode,
              const uint8_t* __restrict__ wimg, const float* __restrict__ hid_b, const float* __restrict__ w_out,
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
-             float* __restrict__ sdf_out, float* __restrict__ terms) {
-    using C = Cfg<H, G>;
+             float* __restrict__ sdf_out, float* __restrict__ terms, const float* __restrict__ w1pe) {
+    using C = Cfg<H, G, PEB>;
     constexpr int CG = C::CG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -391,6 +393,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float4 w0 = w1p[2 * jp], w1 = w1p[2 * jp + 1];
         s_w1xy[jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
         s_w1z[jp] = make_float2(w0.z * kP, w1.z * kP);
+    }
+    if constexpr (PEB > 0) {   // [pair jp][feature f] = (W1[2jp][f], W1[2jp+1][f]) kP
+        float2* s_pe = reinterpret_cast<float2*>(smem + C::OFF_PE);
+        for (int i = threadIdx.x; i < (H / 2) * C::NPE; i += kThreads) {
+            const int jp = i / C::NPE, f = i % C::NPE;
+            s_pe[i] = make_float2(w1pe[(size_t)(2 * jp) * C::NPE + f] * kP, w1pe[(size_t)(2 * jp + 1) * C::NPE + f] * kP);
+        }
     }
     for (int r = threadIdx.x; r < kTileRows; r += kThreads) {   // ones tile: row r = [1, 1, 0 x 14] (bf16)
         uint32_t* o = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (r / 8) * 256 + (r % 8) * 16);
@@ -555,6 +564,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
             const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
             const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
+            if constexpr (PEB > 0) {
+                // PE(p_c) = [p, sin(2^i pi p), cos(2^i pi p)]_{i < PEB} in fp32 (sincospif: exact range
+                // reduction), then the NPE-wide layer-1 dot on FFMA2 (reading E1)
+                float feat[C::NPE];
+                feat[0] = q.x;
+                feat[1] = q.y;
+                feat[2] = q.z;
+#pragma unroll
+                for (int bnd = 0; bnd < PEB; ++bnd) {
+                    const float sc = (float)(1 << bnd);
+                    sincospif(q.x * sc, &feat[3 + 6 * bnd + 0], &feat[3 + 6 * bnd + 3]);
+                    sincospif(q.y * sc, &feat[3 + 6 * bnd + 1], &feat[3 + 6 * bnd + 4]);
+                    sincospif(q.z * sc, &feat[3 + 6 * bnd + 2], &feat[3 + 6 * bnd + 5]);
+                }
+                const float2* s_pe = reinterpret_cast<const float2*>(smem + C::OFF_PE);
+#pragma unroll
+                for (int c = 0; c < C::NH; ++c) {
+#pragma unroll
+                    for (int k = 0; k < C::NCH; ++k) {
+                        const int j0 = c * C::UN + cgi * C::QW + k * kCW;
+                        uint32_t packed[kCW / 2];
+#pragma unroll
+                        for (int i2 = 0; i2 < kCW; i2 += 2) {
+                            const int jp = (j0 + i2) / 2;
+                            float2 x = *reinterpret_cast<const float2*>(b1g + j0 + i2);
+                            if (any_far && bfar) x = make_float2(__ldg(bfar + j0 + i2) * kP, __ldg(bfar + j0 + i2 + 1) * kP);
+#pragma unroll
+                            for (int f = 0; f < C::NPE; ++f) x = ffma2(s_pe[jp * C::NPE + f], make_float2(feat[f], feat[f]), x);
+                            packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
+                        }
+                        tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                    }
+                }
+            } else
 #pragma unroll
             for (int c = 0; c < C::NH; ++c) {
 #pragma unroll
@@ -705,10 +748,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int H, int G, int ACT>
+template <int H, int G, int ACT, int PEB>
 cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s) {
-    using C = Cfg<H, G>;
+    using C = Cfg<H, G, PEB>;
     static bool attr_set = false;
     static int max_groups = 0;   // co-resident CTA groups (clusters) on this device: the persistent grid
     cudaLaunchConfig_t cfg = {};
@@ -723,7 +766,7 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT, PEB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         int dev, n_sm = 0;
         cudaGetDevice(&dev);
@@ -733,7 +776,7 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
         // round-robin over more groups than fit would serialise a second wave
         int clusters = 0;
         cfg.gridDim = dim3((unsigned)(max_groups * C::CG));
-        if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT>, &cfg) == cudaSuccess && clusters > 0)
+        if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT, PEB>, &cfg) == cudaSuccess && clusters > 0)
             max_groups = clusters < max_groups ? clusters : max_groups;
         cudaGetLastError();
         attr_set = true;
@@ -745,9 +788,10 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     if (tiles == 0) return cudaSuccess;
     const long long groups = tiles < max_groups ? tiles : max_groups;
     cfg.gridDim = dim3((unsigned)(groups * C::CG));
-    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
+    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
                               (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,
-                              (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms);
+                              (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms,
+                              (const float*)b.w1pe);
 }
 
 }  // namespace tc
@@ -823,10 +867,27 @@ void mlp_tc_pack_weights(int H, int G, int act, const float* W, const float* hb,
             }
 }
 
+// positional encoding (4 bands) is instantiated for H = 128 only (its layer-1 weights need the smem H = 256
+// does not have)
+template <int HH, int GG, int AA>
+static cudaError_t pe_launch(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
+                             float* sdf_out, bool states_mode, cudaStream_t s) {
+    if constexpr (HH == 128) {
+        if (p.pe_bands == 4) return tc::launch_t<HH, GG, AA, 4>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands) {
+    return pe_bands == 0 || (pe_bands == 4 && H == 128 && n_gemm >= 1 && n_gemm <= 3);
+}
+
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                           float* sdf_out, bool states_mode, cudaStream_t s) {
 #define MPPI_TC_CASE(HH, GG, AA) \
-    if (p.H == HH && p.n_gemm == GG && p.act == AA) return tc::launch_t<HH, GG, AA>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+    if (p.H == HH && p.n_gemm == GG && p.act == AA) \
+        return p.pe_bands == 0 ? tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \
+                               : pe_launch<HH, GG, AA>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
 #define MPPI_TC_ACTS(HH, GG) MPPI_TC_CASE(HH, GG, 0) MPPI_TC_CASE(HH, GG, 1) MPPI_TC_CASE(HH, GG, 2)
 #ifdef MPPI_TC_QUICK   // development builds: the configs[1..4] instantiations only
     MPPI_TC_CASE(128, 2, 1) MPPI_TC_CASE(256, 3, 2)

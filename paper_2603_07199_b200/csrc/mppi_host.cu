@@ -32,7 +32,7 @@ struct Layout {
 };
 
 enum BufId {
-    B_W1P, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
+    B_W1P, B_W1PE, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
     B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_TICK, B_BLKREC, B_REC, B_GATH, B_DIAG, B_FLAGS, B_COUNT
 };
 
@@ -46,6 +46,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     const size_t recw = 4 + 4 * T;
     size_t sz[B_COUNT];
     sz[B_W1P] = 16 * H;
+    sz[B_W1PE] = 4 * H * (size_t)(3 + 6 * c->pe_bands);
     sz[B_W1Z] = 4 * H * Ld;
     sz[B_B1] = 4 * H;
     sz[B_B1F] = 4 * n * H;
@@ -158,6 +159,9 @@ static mppi_status validate(const mppi_config* c) {
     if (c->w_guide != 0.f && !(c->fd_h > 0.f)) return fail(MPPI_ERR_INVALID, "fd_h > 0 with guidance");
     if (c->model != MPPI_MODEL_BASELINE && c->model != MPPI_MODEL_PAPER) return fail(MPPI_ERR_INVALID, "bad model");
     if (c->sdf_provider != MPPI_SDF_MLP && c->sdf_provider != MPPI_SDF_GATE) return fail(MPPI_ERR_INVALID, "bad sdf_provider");
+    if (c->pe_bands != 0 && c->pe_bands != 4) return fail(MPPI_ERR_UNSUPPORTED, "pe_bands must be 0 or 4");
+    if (c->pe_bands && (c->mlp_dtype != MPPI_MLP_BF16 || !mlp_tc_pe_supported(c->hidden, c->n_hidden - 1, c->pe_bands)))
+        return fail(MPPI_ERR_UNSUPPORTED, "positional encoding: bf16 tcgen05 MLP with hidden 128 only");
     if (c->sdf_provider == MPPI_SDF_GATE && (!std::isfinite(c->gate_c) || !(c->gate_tana >= 0.f) || !std::isfinite(c->gate_tana)))
         return fail(MPPI_ERR_INVALID, "gate_c finite, gate_tana >= 0");
     if (c->model == MPPI_MODEL_PAPER) {
@@ -234,6 +238,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     char* base = (char*)ctx->ws;
     Buffers& b = ctx->b;
     b.w1p = (float4*)(base + L.off[B_W1P]);
+    b.w1pe = (float*)(base + L.off[B_W1PE]);
     b.w1z = (float*)(base + L.off[B_W1Z]);
     b.b1 = (float*)(base + L.off[B_B1]);
     b.b1f = (float*)(base + L.off[B_B1F]);
@@ -281,6 +286,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.thrust_max = cfg->thrust_max; p.rate_max = cfg->rate_max;
     p.q_gate = cfg->q_gate; p.q_vis = cfg->q_vis; p.q_sdf = cfg->q_sdf; p.d_safe = cfg->d_safe;
     p.sdf_provider = cfg->sdf_provider; p.gate_c = cfg->gate_c; p.gate_tana = cfg->gate_tana;
+    p.pe_bands = cfg->pe_bands;
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
     ctx->latent_set.assign(cfg->n_ctrl, 0);
 
@@ -357,18 +363,21 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     const int H = c.hidden, Ld = c.latent_dim, G = c.n_hidden - 1;
     if (n_layers != c.n_hidden + 1 || !in_dim || !out_dim || !W || !bvec)
         return fail(MPPI_ERR_INVALID, "n_layers must be n_hidden + 1");
+    const int npe = 3 + 6 * c.pe_bands;   // layer-1 position features (raw p, then the PE bands)
     for (int l = 0; l < n_layers; ++l) {
-        const int ei = l == 0 ? 3 + Ld : H, eo = l == n_layers - 1 ? 1 : H;
+        const int ei = l == 0 ? npe + Ld : H, eo = l == n_layers - 1 ? 1 : H;
         if (in_dim[l] != ei || out_dim[l] != eo) return fail(MPPI_ERR_INVALID, "layer dims do not match the config");
         if (!W[l] || !bvec[l]) return fail(MPPI_ERR_INVALID, "NULL weight pointer");
     }
     const bool bf = c.mlp_dtype == MPPI_MLP_BF16;
     std::vector<float4> w1p(H);
     std::vector<float> w1z((size_t)H * Ld), b1(H), hb((size_t)G * H), wo(H), bo(4, 0.f);
+    std::vector<float> w1pe((size_t)H * npe);
     for (int j = 0; j < H; ++j) {
-        const float* r = W[0] + (size_t)j * (3 + Ld);
+        const float* r = W[0] + (size_t)j * (npe + Ld);
         w1p[j] = make_float4(r[0], r[1], r[2], 0.f);
-        for (int l = 0; l < Ld; ++l) w1z[(size_t)j * Ld + l] = r[3 + l];
+        for (int f = 0; f < npe; ++f) w1pe[(size_t)j * npe + f] = r[f];
+        for (int l = 0; l < Ld; ++l) w1z[(size_t)j * Ld + l] = r[npe + l];
         b1[j] = bvec[0][j];
     }
     std::vector<float> hw((size_t)G * H * H);
@@ -381,6 +390,7 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     cudaStream_t s = ctx->stream;
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1p, w1p.data(), sizeof(float4) * H, cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1pe, w1pe.data(), sizeof(float) * w1pe.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1z, w1z.data(), sizeof(float) * w1z.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.b1, b1.data(), sizeof(float) * H, cudaMemcpyHostToDevice));
     if (G > 0) CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_b, hb.data(), sizeof(float) * hb.size(), cudaMemcpyHostToDevice));

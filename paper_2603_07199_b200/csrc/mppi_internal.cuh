@@ -26,12 +26,14 @@ struct Params {
     // MPPI_SDF_GATE
     int sdf_provider;
     float gate_c, gate_tana;
+    int pe_bands;         // positional encoding bands (0 or 4)
 };
 
 // Device buffers of one context (all inside the workspace).
 struct Buffers {
     // MLP weights
     float4* w1p;          // [H] (W1[j][0..2], unused) layer-1 position columns
+    float* w1pe;          // [H][3 + 6 pe_bands] layer-1 positional-encoding columns (pe_bands > 0)
     float* w1z;           // [H][L] layer-1 latent columns (for the fold)
     float* b1;            // [H]
     float* b1f;           // [n_ctrl][H] folded bias b1' = W1z z + b1
@@ -86,5 +88,6 @@ void mlp_tc_pack_weights(int H, int n_gemm, int act, const float* W, const float
 // else arbitrary rows for mppi_sdf_eval (writes s per row only).
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                           float* sdf_out, bool states_mode, cudaStream_t s);
+bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands);
 
 }  // namespace mppi
