@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     __shared__ float s_half[kSoftminBlock];
     __shared__ float red[kSoftminThreads / 32];
     __shared__ bool s_last;
-    const int bb = blockIdx.y, nblk = gridDim.x;
+    // grid (sample blocks, controllers, T slices): every T slice recomputes the sample block's J, m, S
+    // (identically) and accumulates V only over its own time steps, so the noise-bound phase 2 runs on
+    // gridDim.z times more SMs without adding block records
+    const int bb = blockIdx.y, nblk = gridDim.x, tz = blockIdx.z, nz_t = gridDim.z;
     const int kk = threadIdx.x % kSoftminBlock, half = threadIdx.x / kSoftminBlock;
     const int k = blockIdx.x * kSoftminBlock + kk;
     const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
         if (half == 0 && k < p.K) {
             acc = b.partial[(long long)bb * p.K + k] + acc + s_half[kk];
             J = isfinite(acc) ? acc : INFINITY;
-            b.J[(long long)bb * p.K + k] = J;
+            if (tz == 0) b.J[(long long)bb * p.K + k] = J;
         }
     }
     const float m = block_reduce(J, red, true);
@@ -514,12 +517,13 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     const float S = block_reduce(w, red, false);
     const float S2 = block_reduce(w * w, red, false);
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
-    if (threadIdx.x == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = 0.f; }
+    if (threadIdx.x == 0 && tz == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = 0.f; }
     // ---- phase 2: warp per time step (coalesced over the block's samples), fixed shuffle tree
     const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
     const long long NK = (long long)p.n_ctrl * p.K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int t = warp; t < p.T; t += nw) {
+    const int tsl = (p.T + nz_t - 1) / nz_t, tb = tz * tsl, te = min(p.T, tb + tsl);
+    for (int t = tb + warp; t < te; t += nw) {
         const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     // ---- last block of this controller combines the block records in order
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(b.tickets + bb, 1u) == (unsigned)(nblk - 1);
+    if (threadIdx.x == 0) s_last = atomicAdd(b.tickets + bb, 1u) == (unsigned)(nblk * nz_t - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -603,7 +607,11 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
 }
 
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
-    dim3 grid((p.K + kSoftminBlock - 1) / kSoftminBlock, p.n_ctrl);
+    const int nblk = (p.K + kSoftminBlock - 1) / kSoftminBlock;
+    // T slices so that about 128 blocks run (c1: 8, c2: 2, configs[4]: 1); a slice is >= 8 steps
+    int tsplit = 1;
+    while (tsplit < 8 && (long long)nblk * p.n_ctrl * tsplit * 2 <= 128 && p.T / (tsplit * 2) >= 8) tsplit *= 2;
+    dim3 grid(nblk, p.n_ctrl, tsplit);
     k_softmin<<<grid, kSoftminThreads, 0, s>>>(p, b, write_record ? 1 : 0);
 }
 
