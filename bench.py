@@ -1,9 +1,10 @@
 """Benchmark of one MPPI iteration (the hot path of arxiv 2603.07199) on B200.
 
 python bench.py --gpus N --steps K --warmup W [--impl reference] [--config auto|c0..c4]
-Prints ONE JSON line (rank 0). Workload: configs[2] (K=16384, T=50, 131->256x4->1 SiLU bf16 MLP,
-FD guidance) at N=1; configs[3] (K=131072, T=100, sharded over N ranks, NCCL all-gather of the
-softmin record) for N>1. Inputs are synthetic and seeded (synth/); weights random Kaiming-uniform.
+Prints ONE JSON line (rank 0). Workload (--config auto): configs[3] at every N -- the configuration the
+metric "... at 1/2/4/8 B200" is quoted on: K=131072, T=100, 131->256x4->1 SiLU bf16 MLP, FD guidance,
+the K samples sharded over the N ranks (one NCCL all-gather of the softmin record per iteration), so
+the N=1,2,4,8 lines are the same job (strong scaling). --config c0..c5 runs another configuration. Inputs are synthetic and seeded (synth/); weights random Kaiming-uniform.
 A "step" is one full MPPI iteration: noise -> rollout -> SDF-MLP -> cost/min -> softmin update.
 """
 from __future__ import annotations
@@ -132,7 +133,7 @@ def _oracle_iter(oracle, cfg, Ws, bs):
 
 def pick_config(name, world):
     if name == "auto":
-        name = "c2" if world == 1 else "c3"
+        name = "c3"   # the 1/2/4/8-GPU configuration of the metric, at every N (same job: strong scaling)
     cfg = synth.get_config(name)
     return cfg
 
