@@ -455,8 +455,9 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 // records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
 // U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
-constexpr int kSoftminBlock = 256;     // samples per block
-constexpr int kSoftminThreads = 512;   // two threads per sample in phase 1, 16 warps over t in phase 2
+constexpr int kSoftminThreads = 512;   // 512/SPB threads per sample in phase 1, 16 warps over t in phase 2
+// samples per block: 256, or 512 from K = 65536 on (configs[3]: 256 blocks, one wave at 2 blocks per SM)
+__host__ __device__ constexpr int softmin_spb(int K) { return K >= 65536 ? 512 : 256; }
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
     #pragma unroll
@@ -473,7 +474,9 @@ __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) 
     return r;
 }
 
+template <int kSoftminBlock>
 __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b, int write_record) {
+    constexpr int TPS = kSoftminThreads / kSoftminBlock;   // threads per sample in phase 1 (1 or 2)
     __shared__ float s_w[kSoftminBlock];
     __shared__ float s_half[kSoftminBlock];
     __shared__ float red[kSoftminThreads / 32];
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     // ---- phase 1: two threads per sample, each summing half of the horizon's terms in t order
     float J = INFINITY;
     {
-        const int th = (p.T + 1) / 2, t0 = half * th, t1 = min(p.T, t0 + th);
+        const int th = (p.T + TPS - 1) / TPS, t0 = half * th, t1 = min(p.T, t0 + th);
         float acc = 0.f;
         if (k < p.K) {
             const float* tp = b.terms + (long long)bb * p.T * p.K + k;
@@ -503,10 +506,10 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
             }
             for (; t < t1; ++t) acc += __ldcs(tp + (long long)t * p.K);
         }
-        if (half == 1) s_half[kk] = acc;
+        if (TPS > 1 && half == 1) s_half[kk] = acc;
         __syncthreads();
         if (half == 0 && k < p.K) {
-            acc = b.partial[(long long)bb * p.K + k] + acc + s_half[kk];
+            acc = b.partial[(long long)bb * p.K + k] + acc + (TPS > 1 ? s_half[kk] : 0.f);
             J = isfinite(acc) ? acc : INFINITY;
             if (tz == 0) b.J[(long long)bb * p.K + k] = J;
         }
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
         if (m < INFINITY) {
-#pragma unroll 8
+#pragma unroll 16
             for (int i = lane; i < kn; i += 32) {
                 const float wi = s_w[i];
                 const float4 n = nz[i];
@@ -607,15 +610,17 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
 }
 
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
-    const int nblk = (p.K + kSoftminBlock - 1) / kSoftminBlock;
+    const int spb = softmin_spb(p.K);
+    const int nblk = (p.K + spb - 1) / spb;
     // T slices so that about 128 blocks run (c1: 8, c2: 2, configs[4]: 1); a slice is >= 8 steps
     int tsplit = 1;
     while (tsplit < 8 && (long long)nblk * p.n_ctrl * tsplit * 2 <= 128 && p.T / (tsplit * 2) >= 8) tsplit *= 2;
     dim3 grid(nblk, p.n_ctrl, tsplit);
-    k_softmin<<<grid, kSoftminThreads, 0, s>>>(p, b, write_record ? 1 : 0);
+    if (spb == 512) k_softmin<512><<<grid, kSoftminThreads, 0, s>>>(p, b, write_record ? 1 : 0);
+    else k_softmin<256><<<grid, kSoftminThreads, 0, s>>>(p, b, write_record ? 1 : 0);
 }
 
-int softmin_blocks(int K) { return (K + kSoftminBlock - 1) / kSoftminBlock; }
+int softmin_blocks(int K) { return (K + softmin_spb(K) - 1) / softmin_spb(K); }
 
 // ------------------------------------------------------------------ shard combine (configs[3])
 // m = min_r m_r; S = sum_r S_r e^{-(m_r - m)/lambda}; V = sum_r V_r e^{...}; U* = U + V/S.
