@@ -1,6 +1,7 @@
 """Summarise a round's GPU evidence (gpurun_out/<round>) into the committed profiles/<round>/ files and
 profiles/ncu_mlp_summary.json (the `traffic` source of bench.py). Not part of the library.
-python tools/profile_summary.py r01"""
+python tools/profile_summary.py r01 [SRC_DIR DST_DIR]   (default gpurun_out/r01 -> profiles/r01; on the GPU box
+run it with DST under gpurun_out/ and delete the .ncu-rep files, so the merged-back output stays small)"""
 import csv
 import io
 import json
@@ -40,16 +41,17 @@ def nbytes(v):
 
 def main():
     rnd = sys.argv[1]
-    src = os.path.join(ROOT, "gpurun_out", rnd)
-    dst = os.path.join(ROOT, "profiles", rnd)
+    src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", rnd)
+    dst = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
     for f in os.listdir(src):
-        if f.endswith((".json", ".txt", ".csv")) and not f.startswith("ncu_launch"):
+        if f.endswith((".json", ".txt", ".csv")) and not f.startswith("ncu_launch") and os.path.abspath(src) != os.path.abspath(dst):
             shutil.copy(os.path.join(src, f), dst)
     full = {}
-    summ_path = os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")
+    summ_path = os.path.join(dst, "..", "ncu_mlp_summary.json") if len(sys.argv) > 3 else \
+        os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    for c in ["c2", "c1", "c4"]:
+    for c in ["c3", "c2", "c1", "c4"]:
         rep = os.path.join(src, f"mlp_{c}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -61,15 +63,18 @@ def main():
                        "dram_read_bytes": rd, "dram_write_bytes": wr,
                        "tensor_pipe_active_pct": float(m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"][0]),
                        "xu_pipe_pct": float(m["sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"][0]),
-                       "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0])}
-    rep = os.path.join(src, "small_c2.ncu-rep")
-    if os.path.exists(rep):
-        for name, m in raw(rep):
-            full[f"c2: {name[:60]}"] = m
+                       "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0].replace(",", "")) *
+                                                 {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(
+                                                     m["gpu__time_duration.sum"][1], 1.0)}
+    for c in ["c3", "c2"]:
+        rep = os.path.join(src, f"small_{c}.ncu-rep")
+        if os.path.exists(rep):
+            for name, m in raw(rep):
+                full[f"{c}: {name[:60]}"] = m
     json.dump(full, open(os.path.join(dst, "ncu_full_metrics.json"), "w"), indent=1)
     json.dump(summ, open(summ_path, "w"), indent=1)
     # launch list
-    lf = os.path.join(src, "ncu_launches_c2.csv")
+    lf = os.path.join(src, "ncu_launches_c3.csv")
     if os.path.exists(lf):
         shutil.copy(lf, dst)
         rows = list(csv.reader(open(lf)))
@@ -82,7 +87,7 @@ def main():
         step = {k: v for k, v in d.items() if "mppi" in k or "tc::" in k}
         per_step = sum(sum(v) / len(v) for k, v in step.items() if "k_fold" not in k)
         with open(os.path.join(dst, "ncu_launches_summary.txt"), "w") as f:
-            f.write("# ncu launch list (gpu__time_duration.sum, --clock-control none), bench.py --steps 3 --warmup 3, configs[2]\n")
+            f.write("# ncu launch list (gpu__time_duration.sum, --clock-control none), bench.py --steps 3 --warmup 3, configs[3]\n")
             f.write("# cold-cache, serialised per-launch times: compare SHARES of one step, not absolutes\n")
             f.write(f"{'kernel':60s} launches  mean_us  share_of_step\n")
             for k, v in d.items():
