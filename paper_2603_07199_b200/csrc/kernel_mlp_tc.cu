@@ -64,6 +64,9 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 w
 // (issuer, loader) 32, the four epilogue warpgroups 112: 128 x 32 + 512 x 112 = 640 x 96
 constexpr int kRegsCtl = 32, kRegsEpi = 112;
 constexpr int kCW = 16;         // TMEM columns per epilogue load
+#ifndef MPPI_L1_SMEM
+#define MPPI_L1_SMEM 1
+#endif
 constexpr int kTileRows = 128;
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -331,6 +334,10 @@ struct Cfg {
     static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
+    // H = 128 (one CTA per tile, weights 64 KB): layer 1 writes its activations to a shared-memory A tile
+    // per slot and the first GEMM runs as SS MMAs, so a slot computes layer 1 of its NEXT tile while it
+    // waits for the last GEMM of the current one (layer 1 leaves the tile's MMA <-> epilogue chain)
+    static constexpr bool A1S = CG == 1 && MPPI_L1_SMEM;
     static_assert(A_OFF + H / 2 <= SLOT_COLS && QW % kCW == 0 && RB % 8 == 0, "TMEM / unit layout");
     // smem carve-up (offsets from the 1024-aligned base)
     // hidden-layer biases enter the accumulator through one extra K = 16 MMA per unit: A = a constant
@@ -348,7 +355,9 @@ struct Cfg {
     static constexpr int OFF_PE = OFF_B1 + NSLOT * 4 * H;            // PEB > 0: [H/2][NPE] float2 PE weights, scaled
     static constexpr int OFF_PART = OFF_PE + (PEB > 0 ? (H / 2) * NPE * 8 : 0);   // [NSLOT][COLG][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
-    static constexpr int OFF_BAR = OFF_ROWS + NROWBUF * 16 * kTileRows;
+    static constexpr int OFF_SA = A1S ? (OFF_ROWS + NROWBUF * 16 * kTileRows + 1023) / 1024 * 1024 : 0;
+    static constexpr int SA_BYTES = kTileRows * H * 2;               // [K/64][128 rows][128 B] SW128 K-major
+    static constexpr int OFF_BAR = A1S ? OFF_SA + NSLOT * SA_BYTES : OFF_ROWS + NROWBUF * 16 * kTileRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
     static_assert(SMEM <= 232448, "shared memory budget");
@@ -356,7 +365,7 @@ struct Cfg {
 
 // Barrier slots (8 B each): per tile slot (up to 4) and per query-row buffer (up to 8)
 enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slots]*/, BAR_WLOCAL = 12,
-       BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/ };
+       BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/, BAR_SREADY = 22 /*[slots]: smem layer-1 A tile*/ };
 
 template <int H, int G, int ACT, int PEB>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(bar(BAR_AREADY + i), C::GW * CG);
             mbar_init(bar(BAR_DFREE + i), C::GW * CG);
             mbar_init(bar(BAR_MMA + i), 1);
+            mbar_init(bar(BAR_SREADY + i), C::GW * CG);
         }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::UN);
             const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
-            uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {};
+            uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {}, s_cnt[C::NSLOT] = {};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
             for (long long i0 = 0; i0 < n_my; i0 += C::NSLOT) {
                 const int ns = (int)min((long long)C::NSLOT, n_my - i0);
@@ -471,7 +481,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int h = 0; h < C::NH; ++h)
                         for (int sl = 0; sl < ns; ++sl) {
                             TC_TRACE(0, 0, l, h, sl, i0);
-                            if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
+                            const bool a_smem = C::A1S && l == 0;
+                            if (a_smem) mbar_wait_issuer(bar(BAR_SREADY + sl), (s_cnt[sl]++) & 1);
+                            else if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
                             if (u_cnt[sl] > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u_cnt[sl] - 1) & 1);
                             ++u_cnt[sl];
                             tc_fence_after();
@@ -487,7 +499,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int j = 0; j < H / 16; ++j) {
                                 const int kk = j * 16;
                                 const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
-                                tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
+                                if (a_smem) {
+                                    const uint32_t a_addr = sbase + (uint32_t)(C::OFF_SA + sl * C::SA_BYTES +
+                                                                               (kk / 64) * (kTileRows * 128) + (kk % 64) * 2);
+                                    tc_mma_ss<CG>(d_t, smem_desc_sw128(a_addr), smem_desc_sw128(b_addr), idesc, 1u);
+                                } else {
+                                    tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
+                                }
                             }
                             tc_commit<CG>(bar(BAR_MMA + sl));
                             TC_TRACE(0, 2, l, h, sl, i0);
@@ -542,7 +560,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long row = tile_row0(tile_of(i)) + row_in_tile;
             return row < n_rows ? s_rows[(i % C::NROWBUF) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
         };
-        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> TMEM A of this slot, for tile index i
+        // 16 layer-1 activations (bf16x2) of this thread's row, neurons j0..j0+15 -> the slot's A operand:
+        // TMEM, or (A1S) the shared-memory tile in the SW128 K-major layout of the weight images
+        auto store_a1 = [&](int j0, const uint32_t* packed) {
+            if constexpr (C::A1S) {
+                const int kc = j0 / 64, c0 = (j0 % 64) / 8;
+                const uint32_t rbase = sbase + (uint32_t)(C::OFF_SA + sl * C::SA_BYTES + kc * (kTileRows * 128) + row_in_tile * 128);
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (uint32_t)((((c0 + c) ^ (row_in_tile & 7))) * 16)),
+                                 "r"(packed[4 * c]), "r"(packed[4 * c + 1]), "r"(packed[4 * c + 2]), "r"(packed[4 * c + 3])
+                                 : "memory");
+            } else {
+                tmem_st8(tmem + lane_addr + (uint32_t)(sl * C::SLOT_COLS + C::A_OFF) + (uint32_t)(j0 / 2), packed);
+            }
+        };
+        // layer 1 (CUDA cores): a1 = act(W1p p + b1') -> bf16 -> A operand of this slot, for tile index i
         auto layer1 = [&](long long i) {
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
@@ -550,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tracer) TC_TRACE(trole, 11, 0, 0, sl, t1);
             const float4 q = row_of(i);
             const float2 qx2 = make_float2(q.x, q.x), qy2 = make_float2(q.y, q.y), qz2 = make_float2(q.z, q.z);
-            issue_rows(i + C::NSLOT);   // that buffer was last read by tile i - NSLOT (this group, behind its bar)
+            if constexpr (!C::A1S) issue_rows(i + C::NSLOT);   // buffer last read by tile i - NSLOT (behind its bar)
             const long long row0 = tile_row0(t1);
             const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             if (lo != staged) {   // uniform across the group
@@ -563,7 +596,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
             const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
             const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
-            const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
             if constexpr (PEB > 0) {
                 // PE(p_c) = [p, sin(2^i pi p), cos(2^i pi p)]_{i < PEB} in fp32 (sincospif: exact range
                 // reduction), then the NPE-wide layer-1 dot on FFMA2 (reading E1)
@@ -594,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int f = 0; f < C::NPE; ++f) x = ffma2(s_pe[jp * C::NPE + f], make_float2(feat[f], feat[f]), x);
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
-                        tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                        store_a1(j0, packed);
                     }
                 }
             } else
@@ -626,18 +658,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     }
-                    tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
+                    store_a1(j0, packed);
                 }
             }
             if (tracer) TC_TRACE(trole, 12, 0, 0, sl, t1);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive_sched(BAR_AREADY + sl);
+            if constexpr (C::A1S) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA operand reads
+                __syncwarp();
+                if (lane == 0) arrive_sched(BAR_SREADY + sl);
+            } else {
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_sched(BAR_AREADY + sl);
+            }
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
         issue_rows(sl);
+        if constexpr (C::A1S) issue_rows(sl + C::NSLOT);
         if (sl < n_my) layer1(sl);
         for (long long i = sl; i < n_my; i += C::NSLOT) {
             uint32_t keep[C::NH > 1 ? C::QW / 2 : 1];   // unit-0 activations (bf16x2) until unit 1 is done
@@ -704,6 +743,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (tracer) TC_TRACE(trole, 5, l, h, sl, i);
                 }
+                if constexpr (C::A1S)   // the first GEMM has read the smem A tile: next tile's layer 1
+                    if (l == 0 && i + C::NSLOT < n_my) layer1(i + C::NSLOT);
             }
             // ---- output of this tile: combine column groups, FD pair, write
             const long long tile = tile_of(i);
@@ -731,7 +772,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
-            if (i + C::NSLOT < n_my) layer1(i + C::NSLOT);   // next tile of this slot; overlaps the others' MMAs
+            if constexpr (C::A1S) issue_rows(i + 2 * C::NSLOT);   // this tile's row buffer is free now
+            else if (i + C::NSLOT < n_my) layer1(i + C::NSLOT);   // next tile of this slot; overlaps the others' MMAs
         }
     }
     // ---- teardown

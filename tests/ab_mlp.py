@@ -21,8 +21,9 @@ def child(cfg_name):
     n = cfg0.n_ctrl * cfg0.K * cfg0.T * (2 if cfg0.fd else 1)
     rows = torch.from_numpy(synth.make_query_rows(n, seed=4)).cuda()
     for _ in range(3):
-        ctrl.sdf_eval(rows)
+        out = ctrl.sdf_eval(rows)
     torch.cuda.synchronize()
+    np.save(os.environ["AB_OUT"], out[:1 << 18].float().cpu().numpy())
     smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits", "-lms", "20"],
                            stdout=subprocess.PIPE, text=True)
     ts = []
@@ -52,12 +53,15 @@ def main():
     res = {l: [] for l in libs}
     for _ in range(3):
         for lib in libs:
-            env = dict(os.environ, MPPI_LIB=lib)
+            env = dict(os.environ, MPPI_LIB=lib, AB_OUT=f"/tmp/ab_{os.path.basename(lib)}_{cfg}.npy")
             out = subprocess.run([sys.executable, __file__, "--child", cfg], env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             res[lib].append(json.loads(line[-1]) if line else {"error": out.stderr[-300:]})
+    import numpy as np
+    base = np.load(f"/tmp/ab_{os.path.basename(libs[0])}_{cfg}.npy")
     for lib, rs in res.items():
-        print(os.path.basename(lib), rs)
+        o = np.load(f"/tmp/ab_{os.path.basename(lib)}_{cfg}.npy")
+        print(os.path.basename(lib), rs, "max|d sdf| vs first:", float(np.abs(o - base).max()))
 
 
 if __name__ == "__main__":
