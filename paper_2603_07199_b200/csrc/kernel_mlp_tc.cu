@@ -64,6 +64,9 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 w
 // (issuer, loader) 32, the four epilogue warpgroups 112: 128 x 32 + 512 x 112 = 640 x 96
 constexpr int kRegsCtl = 32, kRegsEpi = 112;
 constexpr int kCW = 16;         // TMEM columns per epilogue load
+#ifndef MPPI_ISSUER_WARP
+#define MPPI_ISSUER_WARP -1   // -1: per configuration (see the issuer); 0 / 1 force lane 0 / the warp form
+#endif
 #ifndef MPPI_L1_SMEM
 #define MPPI_L1_SMEM 1
 #endif
@@ -151,6 +154,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+// One lane of a converged warp (elect.sync): the warp runs the issue loop with warp-uniform values,
+// so the MMA operands stay in uniform registers (no per-MMA R2UR waterfall loop)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -470,7 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // NSLOT tiles in flight (TMEM slots). Per layer and N-half h, one full-K unit per slot, issued slot by
         // slot (X(h0) Y(h0) .. X(h1) Y(h1) ..): while the epilogue drains one slot the tensor pipe works on
         // the others.
-        if (lane == 0 && leader && group < n_tiles) {
+        // H = 256 (CTA pairs): the whole warp walks the schedule and one elected lane issues, so the operands
+        // stay in uniform registers (A/B at configs[2]: -5%); H = 128: lane 0 alone (the warp form +4% at [4])
+        constexpr bool kWarpIssuer = MPPI_ISSUER_WARP < 0 ? CG == 2 : MPPI_ISSUER_WARP != 0;
+        if ((kWarpIssuer || lane == 0) && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::UN);
             const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
             uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {}, s_cnt[C::NSLOT] = {};
@@ -491,23 +504,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
                             const uint32_t a_t = d_t + (uint32_t)C::A_OFF;
                             const uint32_t b_unit = sbase + (uint32_t)((l * C::NH + h) * C::UNIT_BYTES);
-                            // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
-                            tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
-                                          smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
-                                          idesc, 0u);
+                            if (!kWarpIssuer || elect_one()) {
+                                // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
+                                tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
+                                              smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
+                                              idesc, 0u);
 #pragma unroll
-                            for (int j = 0; j < H / 16; ++j) {
-                                const int kk = j * 16;
-                                const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
-                                if (a_smem) {
-                                    const uint32_t a_addr = sbase + (uint32_t)(C::OFF_SA + sl * C::SA_BYTES +
-                                                                               (kk / 64) * (kTileRows * 128) + (kk % 64) * 2);
-                                    tc_mma_ss<CG>(d_t, smem_desc_sw128(a_addr), smem_desc_sw128(b_addr), idesc, 1u);
-                                } else {
-                                    tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
+                                for (int j = 0; j < H / 16; ++j) {
+                                    const int kk = j * 16;
+                                    const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
+                                    if (a_smem) {
+                                        const uint32_t a_addr = sbase + (uint32_t)(C::OFF_SA + sl * C::SA_BYTES +
+                                                                                   (kk / 64) * (kTileRows * 128) + (kk % 64) * 2);
+                                        tc_mma_ss<CG>(d_t, smem_desc_sw128(a_addr), smem_desc_sw128(b_addr), idesc, 1u);
+                                    } else {
+                                        tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
+                                    }
                                 }
+                                tc_commit<CG>(bar(BAR_MMA + sl));
                             }
-                            tc_commit<CG>(bar(BAR_MMA + sl));
+                            if constexpr (kWarpIssuer) __syncwarp();
                             TC_TRACE(0, 2, l, h, sl, i0);
                         }
             }
