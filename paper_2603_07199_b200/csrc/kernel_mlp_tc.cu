@@ -67,6 +67,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_ISSUER_WARP
 #define MPPI_ISSUER_WARP -1   // -1: per configuration (see the issuer); 0 / 1 force lane 0 / the warp form
 #endif
+#ifndef MPPI_EPI_PIPE
+#define MPPI_EPI_PIPE -1   // -1: per configuration (see the epilogue); 0 / 1 force off / on
+#endif
 #ifndef MPPI_L1_SMEM
 #define MPPI_L1_SMEM 1
 #endif
@@ -122,6 +125,9 @@ __device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
         : "=r"(ok) : "r"(a), "r"(parity) : "memory");
     return ok != 0;
 }
+#ifndef MPPI_ISSUER_HINT_NS
+#define MPPI_ISSUER_HINT_NS 100
+#endif
 // Issuer-side wait: try_wait with a 100 ns suspend-time hint (measured 3% faster than the default hint
 // at configs[2]; MPPI_ISSUER_SPIN: spin on test_wait).
 __device__ __forceinline__ void mbar_wait_issuer(uint32_t a, uint32_t parity) {
@@ -136,7 +142,7 @@ __device__ __forceinline__ void mbar_wait_issuer(uint32_t a, uint32_t parity) {
             "{\n\t.reg .pred P1;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
             "selp.b32 %0, 1, 0, P1;\n\t}"
-            : "=r"(ok) : "r"(a), "r"(parity), "n"(100) : "memory");
+            : "=r"(ok) : "r"(a), "r"(parity), "n"(MPPI_ISSUER_HINT_NS) : "memory");
         if (ok) break;
         if (++n > (1u << 26)) __trap();
     }
@@ -486,19 +492,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((kWarpIssuer || lane == 0) && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::UN);
             const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
+            // Barrier phases. H = 256: every slot sees the same sequence per tile (AREADY once per layer, DFREE
+            // before every unit but the first), so they follow from (tile n, l, h) and nothing spills from the
+            // issuer's 32 registers (configs[2] -1.3%). H = 128: per-slot counters (the closed form measured
+            // +15% at configs[1,4] with the lane-0 issuer).
+            constexpr uint32_t kAPerTile = C::A1S ? G - 1 : G;
             uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {}, s_cnt[C::NSLOT] = {};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
             for (long long i0 = 0; i0 < n_my; i0 += C::NSLOT) {
                 const int ns = (int)min((long long)C::NSLOT, n_my - i0);
+                const uint32_t n = (uint32_t)(i0 / C::NSLOT);   // this slot-tile's index: barrier phases below
                 for (int l = 0; l < G; ++l)
                     for (int h = 0; h < C::NH; ++h)
                         for (int sl = 0; sl < ns; ++sl) {
                             TC_TRACE(0, 0, l, h, sl, i0);
                             const bool a_smem = C::A1S && l == 0;
-                            if (a_smem) mbar_wait_issuer(bar(BAR_SREADY + sl), (s_cnt[sl]++) & 1);
-                            else if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
-                            if (u_cnt[sl] > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u_cnt[sl] - 1) & 1);
-                            ++u_cnt[sl];
+                            if constexpr (CG == 2) {
+                                if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
+                                const uint32_t u = (n * G + (uint32_t)l) * C::NH + (uint32_t)h;
+                                if (u > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u - 1) & 1u);
+                            } else {
+                                if (a_smem) mbar_wait_issuer(bar(BAR_SREADY + sl), (s_cnt[sl]++) & 1);
+                                else if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (a_cnt[sl]++) & 1);
+                                if (u_cnt[sl] > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u_cnt[sl] - 1) & 1);
+                                ++u_cnt[sl];
+                            }
                             tc_fence_after();
                             TC_TRACE(0, 1, l, h, sl, i0);
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
@@ -708,11 +726,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
                     const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
                     const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
+                    // H = 256: chunk k + 1's TMEM load is in flight while chunk k is computed (configs[2] -2%;
+                    // H = 128 +2%: load, wait, compute)
+                    constexpr bool kPipe = MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0;
+                    uint32_t accb[kPipe ? 2 : 1][kCW];
+                    if constexpr (kPipe) tmem_ld16(tmem + lane_addr + d_col, accb[0]);
 #pragma unroll
                     for (int k = 0; k < C::NCH; ++k) {
-                        uint32_t acc[kCW];
-                        tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
-                        tmem_wait_ld_regs(acc);
+                        uint32_t(&acc)[kCW] = accb[kPipe ? (k & 1) : 0];
+                        if constexpr (kPipe) {
+                            tmem_wait_ld_regs(acc);
+                            if (k + 1 < C::NCH)
+                                tmem_ld16(tmem + lane_addr + d_col + (uint32_t)((k + 1) * kCW), accb[(k + 1) & 1]);
+                        } else {
+                            tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
+                            tmem_wait_ld_regs(acc);
+                        }
                         if (k == C::NCH - 1) {   // D of the slot may be overwritten now
                             tc_fence_before();
                             __syncwarp();
