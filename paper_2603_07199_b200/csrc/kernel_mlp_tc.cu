@@ -70,6 +70,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_EPI_PIPE
 #define MPPI_EPI_PIPE -1   // -1: per configuration (see the epilogue); 0 / 1 force off / on
 #endif
+#ifndef MPPI_SPLITK
+#define MPPI_SPLITK 1
+#endif
 #ifndef MPPI_L1_SMEM
 #define MPPI_L1_SMEM 1
 #endif
@@ -350,6 +353,10 @@ struct Cfg {
     static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
+    // H = 256: the first unit of a layer (N-half 0) is issued in two K halves. K-half 0 of A (the previous
+    // layer's N-half 0, kept in registers) is written as soon as the previous layer's last MMA has read A,
+    // so those 8 MMAs start when D is free instead of after the whole epilogue of N-half 1.
+    static constexpr bool SPLITK = NH == 2 && MPPI_SPLITK;
     // H = 128 (one CTA per tile, weights 64 KB): layer 1 writes its activations to a shared-memory A tile
     // per slot and the first GEMM runs as SS MMAs, so a slot computes layer 1 of its NEXT tile while it
     // waits for the last GEMM of the current one (layer 1 leaves the tile's MMA <-> epilogue chain)
@@ -381,7 +388,8 @@ struct Cfg {
 
 // Barrier slots (8 B each): per tile slot (up to 4) and per query-row buffer (up to 8)
 enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slots]*/, BAR_WLOCAL = 12,
-       BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/, BAR_SREADY = 22 /*[slots]: smem layer-1 A tile*/ };
+       BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/, BAR_SREADY = 22 /*[slots]: smem layer-1 A tile*/,
+       BAR_AK0 = 26 /*[slots]: K-half 0 of A written (SPLITK)*/ };
 
 template <int H, int G, int ACT, int PEB>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -440,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(bar(BAR_DFREE + i), C::GW * CG);
             mbar_init(bar(BAR_MMA + i), 1);
             mbar_init(bar(BAR_SREADY + i), C::GW * CG);
+            mbar_init(bar(BAR_AK0 + i), C::GW * CG);
         }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             TC_TRACE(0, 0, l, h, sl, i0);
                             const bool a_smem = C::A1S && l == 0;
                             if constexpr (CG == 2) {
-                                if (h == 0) mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
+                                if (h == 0) mbar_wait_issuer(bar(C::SPLITK ? BAR_AK0 + sl : BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
                                 const uint32_t u = (n * G + (uint32_t)l) * C::NH + (uint32_t)h;
                                 if (u > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u - 1) & 1u);
                             } else {
@@ -522,13 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
                             const uint32_t a_t = d_t + (uint32_t)C::A_OFF;
                             const uint32_t b_unit = sbase + (uint32_t)((l * C::NH + h) * C::UNIT_BYTES);
-                            if (!kWarpIssuer || elect_one()) {
-                                // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
-                                tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
-                                              smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
-                                              idesc, 0u);
+                            auto issue_k = [&](int j_lo, int j_hi) {   // K steps [16 j_lo, 16 j_hi) of the unit
 #pragma unroll
                                 for (int j = 0; j < H / 16; ++j) {
+                                    if (j < j_lo || j >= j_hi) continue;
                                     const int kk = j * 16;
                                     const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
                                     if (a_smem) {
@@ -539,6 +545,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
                                     }
                                 }
+                            };
+                            // SPLITK: N-half 0 starts on K-half 0 of A; K-half 1 waits for the whole epilogue
+                            const int j_mid = C::SPLITK && h == 0 ? H / 32 : H / 16;
+                            if (!kWarpIssuer || elect_one()) {
+                                // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
+                                tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
+                                              smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
+                                              idesc, 0u);
+                                issue_k(0, j_mid);
+                            }
+                            if (C::SPLITK && h == 0) {
+                                if constexpr (kWarpIssuer) __syncwarp();
+                                mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
+                                tc_fence_after();
+                            }
+                            if (!kWarpIssuer || elect_one()) {
+                                issue_k(j_mid, H / 16);
                                 tc_commit<CG>(bar(BAR_MMA + sl));
                             }
                             if constexpr (kWarpIssuer) __syncwarp();
@@ -694,6 +717,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     store_a1(j0, packed);
                 }
+                if (C::SPLITK && c == 0) {   // K-half 0 of the first GEMM's A is complete
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive_sched(BAR_AK0 + sl);
+                }
             }
             if (tracer) TC_TRACE(trole, 12, 0, 0, sl, t1);
             if constexpr (C::A1S) {
@@ -726,6 +755,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
                     const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
                     const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
+                    if (C::SPLITK && !last && h == C::NH - 1) {
+                        // the layer's last MMA has read A: N-half 0's activations -> K-half 0 of the next A now
+#pragma unroll
+                        for (int k = 0; k < C::NCH; ++k)
+                            tmem_st8(tmem + lane_addr + a_col + (uint32_t)((cgi * C::QW + k * kCW) / 2), &keep[k * (kCW / 2)]);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_sched(BAR_AK0 + sl);
+                    }
                     // H = 256: chunk k + 1's TMEM load is in flight while chunk k is computed (configs[2] -2%;
                     // H = 128 +2%: load, wait, compute)
                     constexpr bool kPipe = MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0;
@@ -762,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 for (int i2 = 0; i2 < kCW / 2; ++i2) keep[k * (kCW / 2) + i2] = packed[i2];
                             } else {
                                 // every unit of this layer done: A of the slot is dead -> next input
-                                if constexpr (C::NH > 1)
+                                if constexpr (C::NH > 1 && !C::SPLITK)
                                     tmem_st8(tmem + lane_addr + a_col + (uint32_t)((j0 - C::UN) / 2), &keep[k * (kCW / 2)]);
                                 tmem_st8(tmem + lane_addr + a_col + (uint32_t)(j0 / 2), packed);
                             }
