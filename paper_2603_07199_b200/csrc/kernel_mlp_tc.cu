@@ -17,12 +17,17 @@
 // CTA keeps HALF of every weight matrix resident (192 KB for 3 GEMM layers) and its own 128 rows in
 // TMEM; only the pair's leader issues MMAs. H = 128 (configs[1,4]) runs one CTA per tile (cta_group::1,
 // M = 128) with all weights resident (<= 96 KB).
-// Per tile and GEMM layer the MMA work is four units (N-half h, K-half c), ordered h0c0 h0c1 h1c0 h1c1:
-// the epilogue of N-half 0 overlaps the MMAs of N-half 1, and the next layer's K-half-0 MMAs overlap
-// the epilogue of N-half 1. TMEM columns: D [0, H) fp32 accumulator; A0 [H, 3H/2) and
-// A1 [3H/2, 2H) bf16 activations (two per 32-bit column), alternating per layer.
-// Warp roles: warp 0 = TMEM allocator + MMA issuer (one thread of the leader CTA); warp 1 = weight
-// loader; warps 4..19 = epilogue (warp w owns TMEM lanes 32 (w%4)..+31 and one column quarter of a unit).
+// Two tiles in flight per CTA (TMEM slots X, Y: D = 128 fp32 columns + A = H/2 bf16x2 columns each).
+// Per layer the MMA work is one full-K unit per N-half h (N = 128) and slot, issued X(h0) Y(h0) X(h1)
+// Y(h1): the epilogue of one slot overlaps the MMAs of the other. D is released as soon as the epilogue
+// has loaded it; the N-half-0 activations wait in registers until the layer's last MMA has read A. At
+// H = 256 the next layer's N-half-0 unit is issued in two K halves: K-half 0 as soon as those kept
+// activations are stored (and D is free), K-half 1 after the N-half-1 epilogue.
+// H = 128: layer 1 writes a shared-memory A tile and the first GEMM runs as SS MMAs, so each slot
+// computes layer 1 of its next tile while its last GEMM runs.
+// Warp roles: warp 0 = TMEM allocator + MMA issuer (the leader CTA; H = 256: the whole warp, one
+// elected lane issues); warp 1 = weight loader; warps 4..19 = epilogue, two groups of 8 (one per
+// slot; warp w owns TMEM lanes 32 (w%4)..+31 and one column half of a unit).
 #include <cuda_bf16.h>
 #include <stdint.h>
 
