@@ -531,14 +531,26 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
         if (m < INFINITY) {
-#pragma unroll 16
-            for (int i = lane; i < kn; i += 32) {
-                const float wi = s_w[i];
-                const float4 n = nz[i];
-                v0 = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v0);
-                v1 = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v1);
-                v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
-                v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
+            // all of this lane's noise loads for step t first (kSoftminBlock / 32 in flight), then the sums in
+            // sample order (the loads interleaved with the FMA chains ran at ~0.5 TB/s)
+            constexpr int PER = kSoftminBlock / 32;
+            float4 nv[PER];
+#pragma unroll
+            for (int r = 0; r < PER; ++r) {
+                const int i = lane + 32 * r;
+                nv[r] = i < kn ? __ldcs(nz + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int r = 0; r < PER; ++r) {
+                const int i = lane + 32 * r;
+                if (i < kn) {
+                    const float wi = s_w[i];
+                    const float4 n = nv[r];
+                    v0 = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v0);
+                    v1 = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v1);
+                    v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
+                    v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
+                }
             }
         }
 #pragma unroll
