@@ -139,6 +139,19 @@ def test_multi_controller_gates():
     _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
 
 
+@pytest.mark.parametrize("name,over", [
+    ("c4s", {"n_ctrl": 5, "K": 36, "T": 3}),   # H = 128: 216 rows per controller, 128-row tiles straddle two
+    ("c2s", {"n_ctrl": 3, "K": 40, "T": 3}),   # H = 256: 240 rows per controller, 256-row pair tiles straddle
+])
+def test_tiles_across_controllers(name, over):
+    """Tiles whose rows belong to two controllers: the layer-1 folded bias b1' switches inside the tile
+    (the kernel's per-row far-controller path), at both MLP widths."""
+    cfg, Ws, bs, inp, ctrl = gh.setup(name, **over)
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
+
+
 def test_ragged_tiles():
     """State count not a multiple of the 64-state tile; K not a multiple of a warp."""
     cfg, Ws, bs, inp, ctrl = gh.setup("c1s", K=37, T=3)
