@@ -107,12 +107,14 @@ def cpu_baseline(cfg, seconds_target=15.0):
     oracle.build()
     cores = len(os.sched_getaffinity(0))
     Ws, bs = synth.make_weights(cfg)
-    oc_probe = cfg.replace(n_ctrl=1, K=8)
-    # probe the rate, then size the sample for ~seconds_target of CPU work
+    # probe the rate with 2 samples per core (all cores busy, as in the measured run), then size the
+    # sample for ~seconds_target of CPU work
+    k_p = min(cfg.K, 2 * cores)
+    oc_probe = cfg.replace(n_ctrl=1, K=k_p)
     t0 = time.perf_counter()
     _oracle_iter(oracle, oc_probe, Ws, bs)
     dt = time.perf_counter() - t0
-    k_s = int(max(8, min(cfg.K, 8 * seconds_target / max(dt, 1e-6))))
+    k_s = int(max(8, min(cfg.K, k_p * seconds_target / max(dt, 1e-6))))
     k_s = max(cores, (k_s // cores) * cores)
     sc = cfg.replace(n_ctrl=1, K=k_s)
     t0 = time.perf_counter()
@@ -311,7 +313,9 @@ def main():
                             f"that pass took {float(np.mean(prof_ms)):.4f} ms/step"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if plan.mode != "replica" else "weak", "vs_baseline": None, "dtype": "bf16",
+            # the partition this config uses at N > 1 (configs[3] samples, configs[4] controllers: total work
+            # fixed = strong; others: independent replicas = weak), the same key at N = 1 as in the scaling run
+            "scaling": "strong" if shard.plan(cfg, 2, 0).mode != "replica" else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded; random Kaiming-uniform MLP weights, N(0,1) latents)",
             "config": {"workload": workload_name(cfg, world), "n_ctrl": cfg.n_ctrl, "K": cfg.K, "T": cfg.T,
                        "per_rank": {"n_ctrl": lcfg.n_ctrl, "K": lcfg.K},
