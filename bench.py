@@ -100,7 +100,7 @@ def ncu_traffic(cfg_name):
         return None
 
 
-def cpu_baseline(cfg, seconds_target=25.0):
+def cpu_baseline(cfg, seconds_target=40.0):
     """The oracle as it stands, on this host's cores, over a bounded sample of the same workload:
     the first k_s samples of controller 0 (same T, MLP, costs), one full oracle iteration."""
     import oracle
