@@ -133,6 +133,13 @@ def _oracle_iter(oracle, cfg, Ws, bs):
                        want_queries=False)
 
 
+def scaling_of(cfg) -> str:
+    """The partition the config uses at N > 1 (configs[3]: samples, configs[4]: controllers -- total work
+    fixed, strong; others: independent replicas, weak); the same key at every N, both arms."""
+    from paper_2603_07199_b200 import shard
+    return "strong" if shard.plan(cfg, 2, 0).mode != "replica" else "weak"
+
+
 def pick_config(name, world):
     if name == "auto":
         name = "c3"   # the 1/2/4/8-GPU configuration of the metric, at every N (same job: strong scaling)
@@ -154,7 +161,7 @@ def run_reference(args, world, rank):
     v = info["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (bf16-emulated MLP)", "data": "synthetic",
+            "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "f64 (bf16-emulated MLP)", "data": "synthetic",
             "config": {"workload": workload_name(cfg, 1) + " (oracle, bounded sample per step)"},
             "cpu_baseline": info, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -315,7 +322,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             # the partition this config uses at N > 1 (configs[3] samples, configs[4] controllers: total work
             # fixed = strong; others: independent replicas = weak), the same key at N = 1 as in the scaling run
-            "scaling": "strong" if shard.plan(cfg, 2, 0).mode != "replica" else "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded; random Kaiming-uniform MLP weights, N(0,1) latents)",
             "config": {"workload": workload_name(cfg, world), "n_ctrl": cfg.n_ctrl, "K": cfg.K, "T": cfg.T,
                        "per_rank": {"n_ctrl": lcfg.n_ctrl, "K": lcfg.K},
