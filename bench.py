@@ -100,12 +100,19 @@ def ncu_traffic(cfg_name):
         return None
 
 
-def cpu_baseline(cfg, seconds_target=40.0):
+def cpu_baseline(cfg, seconds_target=40.0, threads=None):
     """The oracle as it stands, on this host's cores, over a bounded sample of the same workload:
-    the first k_s samples of controller 0 (same T, MLP, costs), one full oracle iteration."""
+    the first k_s samples of controller 0 (same T, MLP, costs), one full oracle iteration. threads=1 runs
+    it single-threaded (OMP_NUM_THREADS=1 in a subprocess; BASELINE.md §3 plans both runs)."""
+    if threads == 1:
+        env = dict(os.environ, OMP_NUM_THREADS="1")
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--_cpu-baseline-child", cfg.name,
+                            str(seconds_target)], capture_output=True, text=True, env=env, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        return out, out.pop("_dt")
     import oracle
     oracle.build()
-    cores = len(os.sched_getaffinity(0))
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     Ws, bs = synth.make_weights(cfg)
     # probe the rate with 2 samples per core (all cores busy, as in the measured run), then size the
     # sample for ~seconds_target of CPU work
@@ -122,7 +129,7 @@ def cpu_baseline(cfg, seconds_target=40.0):
     dt = time.perf_counter() - t0
     return {"value": k_s * cfg.T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"one oracle iteration over {k_s} of {cfg.K} samples x T={cfg.T} of {cfg.name} "
-                      f"(controller 0), {dt:.1f} s, OpenMP over samples"}, dt
+                      f"(controller 0), {dt:.1f} s, " + ("single thread" if cores == 1 else "OpenMP over samples")}, dt
 
 
 def _oracle_iter(oracle, cfg, Ws, bs):
@@ -167,55 +174,33 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="auto")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, world, rank)
-
-    import torch
-    import torch.distributed as dist
-    from paper_2603_07199_b200 import Controller, nccl_unique_id, build as b
-    b.build()
-    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = pick_config(args.config, world)
-    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
-
-    # ---- shard (configs[3]: samples + one NCCL all-gather; configs[4]: controllers; others: replicas)
-    from paper_2603_07199_b200 import shard
-    plan = shard.plan(cfg, world, rank)
-    sharded = plan.sharded
-    nccl_id = None
-    if sharded:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+def make_controller(cfg, plan, world, rank, local, nccl_id):
+    from paper_2603_07199_b200 import Controller
     lcfg = cfg.replace(K=plan.K_local, n_ctrl=plan.n_ctrl_local)
-    ctrl = Controller(lcfg, device=local, noise_mode="device", world_size=world if sharded else 1,
-                      rank=rank if sharded else 0, K_global=plan.K_global, k_offset=plan.k_offset, nccl_id=nccl_id)
+    ctrl = Controller(lcfg, device=local, noise_mode="device", world_size=world if plan.sharded else 1,
+                      rank=rank if plan.sharded else 0, K_global=plan.K_global, k_offset=plan.k_offset,
+                      nccl_id=nccl_id, ctrl_offset=plan.ctrl_offset)
     Ws, bs = synth.make_weights(cfg)
-    ctrl.set_sdf_weights(Ws, bs)
+    if cfg.sdf_provider == 0:
+        ctrl.set_sdf_weights(Ws, bs)
     csl = slice(plan.ctrl_offset, plan.ctrl_offset + plan.n_ctrl_local)
     Tq = synth.make_query_transforms(cfg)[csl]
     ctrl.set_latent(synth.make_latents(cfg)[csl], Tq)
     ctrl.set_nominal(synth.make_nominal(cfg)[csl])
-    x0_h, goal_h = synth.make_x0(cfg)[csl], synth.make_goals(cfg)[csl]
+    return ctrl, lcfg, csl, Tq
+
+
+def time_config(cfg, plan, world, rank, local, nccl_id, steps, warmup, with_e2e=True, dist=None):
+    """Device-timed steps of one configuration (the step graph, L2 flushed before every step, latent
+    redrawn every 5 steps off the timed region), the SDF-MLP launch time of a second profiled pass, the
+    per-stage breakdown, and (with_e2e) the end-to-end rate through mppi_step + mppi_get_controls."""
+    import torch
+    ctrl, lcfg, csl, Tq = make_controller(cfg, plan, world, rank, local, nccl_id)
     dev = torch.device("cuda", local)
+    x0_h, goal_h = synth.make_x0(cfg)[csl], synth.make_goals(cfg)[csl]
     x0_d = torch.from_numpy(x0_h).to(dev)
     goal_d = torch.from_numpy(goal_h).to(dev)
-    n_frames = 1 + (args.warmup + 2 * args.steps + 4) // 5 + 1
+    n_frames = 1 + (warmup + 2 * steps + 4) // 5 + 1
     latents = [synth.make_latents(cfg, frame=f)[csl] for f in range(n_frames)]
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
@@ -246,25 +231,25 @@ def main():
     # the sampler starts before the warm-up (nvidia-smi needs a few hundred ms to produce samples) and
     # stops right after the timed steps
     with ClockSampler(local) as clk:
-        for i in range(args.warmup):
+        for i in range(warmup):
             one_step(i, False)
         time.sleep(0.3)
-        for i in range(args.warmup):
+        for i in range(warmup):
             one_step(i, False)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        for i in range(args.warmup, args.warmup + args.steps):
+        for i in range(warmup, warmup + steps):
             ms, _ = one_step(i, True)
             step_ms.append(ms)
         torch.cuda.synchronize()
     # roofline pass: events around the SDF-MLP launch (same inputs, same L2 flush, K steps)
     ctrl.set_profiling(1)
     for i in range(2):
-        one_step(args.warmup + args.steps + i, False)
+        one_step(warmup + steps + i, False)
     prof_ms = []
-    for i in range(args.steps):
-        ms, kt = one_step(args.warmup + args.steps + 2 + i, "kernels")
+    for i in range(steps):
+        ms, kt = one_step(warmup + steps + 2 + i, "kernels")
         prof_ms.append(ms)
         ktimes.append(kt)
     ctrl.set_profiling(0)
@@ -276,48 +261,124 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    # rollout-steps of the whole job (all ranks); replicas each run the full configuration
-    units_per_step = cfg.n_ctrl * cfg.K * cfg.T * (world if plan.mode == "replica" else 1)
-    value = units_per_step * args.steps / (total_ms * 1e-3)
+    out = dict(ctrl=ctrl, lcfg=lcfg, step_ms=step_ms, ms_per_step=total_ms / steps, stage_kt=stage_kt,
+               mlp_ms=float(np.mean(np.array(ktimes)[:, 2])), prof_ms=float(np.mean(prof_ms)), clocks=clk.summary())
+    if with_e2e:
+        # ---- end to end through the public API with host buffers (pinned staging H2D, D2H of U*)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(3):
+            ctrl.step(x0_h, goal_h, 1000 + i)
+            ctrl.get_controls()
+        t0 = time.perf_counter()
+        for i in range(steps):
+            ctrl.step(x0_h, goal_h, 2000 + i)
+            ctrl.get_controls()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        out["e2e_s"] = e2e_s
+    return out
 
-    # ---- end to end through the public API with host buffers (pinned staging H2D, D2H of U*)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ctrl.set_profiling(False)
-    for i in range(3):
-        ctrl.step(x0_h, goal_h, 1000 + i)
-        ctrl.get_controls()
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        ctrl.step(x0_h, goal_h, 2000 + i)
-        U, u0 = ctrl.get_controls()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = units_per_step * args.steps / e2e_s
 
-    kt = stage_kt                                  # per-stage ms (noise, rollout, mlp, softmin, exchange)
-    peaks, peak_src = measured_peaks()
+def roofline_of(cfg, lcfg, mlp_ms, ms_per_step, peaks):
     rows = lcfg.n_ctrl * lcfg.K * lcfg.T * (2 if cfg.fd else 1)
     flop = mlp_flops_per_row(cfg) * rows
-    mlp_ms = float(np.mean(np.array(ktimes)[:, 2]))
     achieved = flop / (mlp_ms * 1e-3) / 1e12
+    return dict(rows=rows, flop=flop, achieved=achieved, frac=achieved / peaks["bf16_tflops"],
+                frac_sustained=achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                tensor_floor_ms=flop / (peaks["bf16_tflops"] * 1e12) * 1e3, mlp_share=mlp_ms / ms_per_step)
+
+
+def extra_line(name, steps, warmup, local, peaks):
+    """A driver-observed figure for another configuration (one GPU, same timing rules, no e2e)."""
+    from paper_2603_07199_b200 import shard
+    cfg = synth.get_config(name)
+    plan = shard.plan(cfg, 1, 0)
+    r = time_config(cfg, plan, 1, 0, local, None, steps, warmup, with_e2e=False)
+    rf = roofline_of(cfg, r["lcfg"], r["mlp_ms"], r["ms_per_step"], peaks)
+    r["ctrl"].close()
+    units = cfg.n_ctrl * cfg.K * cfg.T
+    d = {"workload": workload_name(cfg, 1), "ms_per_step": r["ms_per_step"],
+         "median_ms": float(np.median(r["step_ms"])), "p99_ms": float(np.percentile(r["step_ms"], 99)),
+         "rollout_steps_per_s": units / (r["ms_per_step"] * 1e-3),
+         "sdf_mlp_ms": r["mlp_ms"], "sdf_mlp_tflops": rf["achieved"], "frac_of_burst_bf16": rf["frac"],
+         "tensor_floor_ms": rf["tensor_floor_ms"], "mlp_share_of_step": rf["mlp_share"],
+         "stage_ms": {k: float(v) for k, v in zip(["noise_shift(fused)", "rollout", "sdf_mlp", "softmin_update",
+                                                   "exchange"], r["stage_kt"])},
+         "clocks": r["clocks"], "steps": steps, "warmup": warmup}
+    if cfg.n_ctrl > 1:
+        d["controller_iterations_per_s"] = cfg.n_ctrl / (r["ms_per_step"] * 1e-3)
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs' driver-observed figures")
+    ap.add_argument("--_cpu-baseline-child", nargs=2, default=None, help=argparse.SUPPRESS)
+    args = ap.parse_args()
+    if args._cpu_baseline_child:
+        cfg = synth.get_config(args._cpu_baseline_child[0])
+        out, dt = cpu_baseline(cfg, seconds_target=float(args._cpu_baseline_child[1]))
+        out["_dt"] = dt
+        print(json.dumps(out), flush=True)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_07199_b200 import nccl_unique_id, build as b
+    b.build()
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = pick_config(args.config, world)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    # ---- shard (configs[3]: samples + one NCCL all-gather; configs[4]: controllers; others: replicas)
+    from paper_2603_07199_b200 import shard
+    plan = shard.plan(cfg, world, rank)
+    nccl_id = None
+    if plan.sharded:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    r = time_config(cfg, plan, world, rank, local, nccl_id, args.steps, args.warmup, with_e2e=True, dist=dist)
+    ctrl, lcfg, ms_per_step = r["ctrl"], r["lcfg"], r["ms_per_step"]
+    # rollout-steps of the whole job (all ranks); replicas each run the full configuration
+    units_per_step = cfg.n_ctrl * cfg.K * cfg.T * (world if plan.mode == "replica" else 1)
+    value = units_per_step / (ms_per_step * 1e-3)
+    e2e_value = units_per_step * args.steps / r["e2e_s"]
+
+    kt = r["stage_kt"]                             # per-stage ms (noise, rollout, mlp, softmin, exchange)
+    peaks, peak_src = measured_peaks()
+    rf = roofline_of(cfg, lcfg, r["mlp_ms"], ms_per_step, peaks)
     traffic = ncu_traffic(cfg.name)
-    roofline = {"bound": "tensor", "kernel": "k_mlp_tc (fused SDF-MLP, tcgen05)", "achieved": achieved,
-                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
-                "frac_sustained": achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+    roofline = {"bound": "tensor", "kernel": "k_mlp_tc (fused SDF-MLP, tcgen05)", "achieved": rf["achieved"],
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": rf["frac"],
+                "frac_sustained": rf["frac_sustained"],
                 "peak_source": f"{peak_src} bf16 dense (burst)", "traffic": traffic,
-                "algorithmic_flop_per_launch": flop, "flop_per_row": mlp_flops_per_row(cfg), "rows_per_launch": rows,
-                "mlp_share_of_step": mlp_ms / ms_per_step,
+                "algorithmic_flop_per_launch": rf["flop"], "flop_per_row": mlp_flops_per_row(cfg),
+                "rows_per_launch": rf["rows"], "mlp_share_of_step": rf["mlp_share"],
                 "stage_ms": {k: float(v) for k, v in zip(["noise_shift(fused)", "rollout", "sdf_mlp", "softmin_update", "exchange"], kt)},
                 "stage_ms_note": "separate 3-step pass with events at every stage boundary (~6 us each)",
                 "measured": "CUDA events in the step graph around the SDF-MLP launch, over a second pass of the "
                             "same K steps right after the timed region (whose graph has no event nodes); "
-                            f"that pass took {float(np.mean(prof_ms)):.4f} ms/step"}
+                            f"that pass took {r['prof_ms']:.4f} ms/step"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             # the partition this config uses at N > 1 (configs[3] samples, configs[4] controllers: total work
@@ -331,21 +392,38 @@ def main():
                        "parallelism": {"samples": f"samples sharded x{world} + NCCL all-gather of the softmin record",
                                        "controllers": f"controllers x{world}, no communication",
                                        "replica": "single GPU" if world == 1 else f"{world} independent replicas"}[plan.mode]},
-            "latency_ms": {"mean": ms_per_step, "median": float(np.median(step_ms)),
-                           "p99": float(np.percentile(step_ms, 99))},
+            "latency_ms": {"mean": ms_per_step, "median": float(np.median(r["step_ms"])),
+                           "p99": float(np.percentile(r["step_ms"], 99))},
             "roofline": roofline,
-            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": 1e3 * r["e2e_s"] / args.steps,
                     "h2d_bytes_per_step": lcfg.n_ctrl * 13 * 4 + 8, "d2h_bytes_per_step": lcfg.n_ctrl * (cfg.T * 16 + 4),
                     "note": "mppi_step (pinned staging H2D of x0, goal) + mppi_get_controls (D2H of U*), wall clock"},
             "gpu_launches": args.steps * ctrl.kernels_per_step(),
-            "clocks": clk.summary()}
+            "clocks": r["clocks"]}
+    ctrl.close()
+    if world == 1 and not args.no_extra and args.config == "auto":
+        # driver-observed figures for the other configurations in the same invocation:
+        # north_star's target (configs[2] < 1 ms on one B200) and configs[1], [4] and the paper-model c5
+        ns = extra_line("c2", max(args.steps, 20), args.warmup, local, peaks)
+        ns.update({"target_ms": 1.0, "target_met": ns["ms_per_step"] < 1.0,
+                   "tensor_pipe_pct_ncu": (json.load(open(os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")))
+                                           .get("c2", {}).get("tensor_pipe_active_pct")
+                                           if os.path.exists(os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")) else None),
+                   "tensor_pipe_note": "ncu --set full of the same kernel (profiles/ncu_mlp_summary.json); "
+                                       "never a number taken under the profiler for time"})
+        line["north_star_c2"] = ns
+        line["other_configs"] = {n: extra_line(n, max(args.steps, 20), args.warmup, local, peaks)
+                                 for n in ("c1", "c4", "c5")}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)[0]
+        try:
+            line["cpu_baseline_single_thread"] = cpu_baseline(cfg, seconds_target=15.0, threads=1)[0]
+        except Exception as e:   # reported, never fatal for the GPU line
+            line["cpu_baseline_single_thread"] = {"unavailable": str(e)[:200]}
     elif rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = None
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctrl.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define MPPI_ABI_VERSION 2
+#define MPPI_ABI_VERSION 3
 
 typedef struct mppi_ctx mppi_ctx;
 typedef int32_t mppi_status;
@@ -103,14 +103,24 @@ typedef struct {
                                                    0, or 4 (bf16 MLP with hidden 128): layer 1 reads
                                                    [p, sin(2^i pi p), cos(2^i pi p) (i < 4) | z], i.e.
                                                    in_dim[0] = 3 + 6 pe_bands + latent_dim (E1) */
+    /* ABI 3 */
+    int64_t ctrl_offset;                        /* global index of this context's first controller when the
+                                                   controllers of one job are split over contexts/ranks
+                                                   (configs[4]); keys the device noise, so the split job draws
+                                                   the unsplit job's samples. 0 otherwise */
 } mppi_config;
 
 /* Bytes of device workspace mppi_create() needs for this config (0 if the config is invalid). */
 size_t mppi_workspace_bytes(const mppi_config* cfg);
 
-/* Validate cfg, bind the workspace (NULL: library-allocated), create the context. With world_size > 1
- * and a non-NULL nccl_unique_id this is collective over all ranks (ncclCommInitRank). */
+/* Validate cfg, bind the workspace (NULL: library-allocated), create the context: one MPPI controller
+ * state (U*, weights, latent cache) per controller of the batch. With
+ * world_size > 1 and a non-NULL nccl_unique_id this is collective over all ranks (ncclCommInitRank).
+ * Errors: MPPI_ERR_INVALID / MPPI_ERR_UNSUPPORTED (bad or unbuilt config; *out = NULL), MPPI_ERR_OOM,
+ * MPPI_ERR_CUDA, MPPI_ERR_NCCL. */
 mppi_status mppi_create(const mppi_config* cfg, void* d_workspace, size_t ws_bytes, mppi_ctx** out);
+/* Wait for the context's queued work, then release everything it owns (not a caller workspace).
+ * NULL is a no-op. Always MPPI_OK; also valid on a poisoned context. */
 mppi_status mppi_destroy(mppi_ctx* ctx);
 
 /* Fill out128 with a fresh ncclUniqueId (rank 0; the caller broadcasts it, e.g. torch.distributed). */
@@ -129,6 +139,19 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
  * controller from arrays z [n_ctrl][L] and T_q [n_ctrl][12]. Requires weights. */
 mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q);
 
+/* Latent cache with object permanence (§IV-B3: "we cache the latest valid latent code
+ * and its corresponding camera pose ... under visual occlusion the SDF is queried in the cached frame").
+ * valid != 0: a valid depth frame -- as mppi_set_latent, and t_frame (caller's clock, s) is recorded.
+ * valid == 0: an invalid/occluded frame -- nothing is uploaded; the cached (z, T_q) of the last valid
+ * frame stays in use (z / T_q may be NULL). Either way the frame is counted. Before the first valid frame
+ * of a controller, stepping returns MPPI_ERR_NOT_READY. ctrl = -1: every controller (arrays as above). */
+mppi_status mppi_set_latent_frame(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q, double t_frame,
+                                  int32_t valid);
+/* Cache status per controller: out_t [n_ctrl] = t_frame of the cached (last valid) frame (NaN when it came
+ * from mppi_set_latent), out_steps [n_ctrl] = mppi_step calls since it was set (the latent's age in
+ * iterations), out_invalid [n_ctrl] = invalid frames seen since then. Any pointer may be NULL. */
+mppi_status mppi_get_latent_status(mppi_ctx* ctx, double* out_t, int64_t* out_steps, int64_t* out_invalid);
+
 /* Nominal sequence U* [T][4] for controller ctrl (ctrl = -1: [n_ctrl][T][4]); resets the warm start. */
 mppi_status mppi_set_nominal(mppi_ctx* ctx, int32_t ctrl, const float* U);
 
@@ -146,9 +169,10 @@ mppi_status mppi_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_
 mppi_status mppi_step_device(mppi_ctx* ctx, const float* d_x0, const float* d_goal, uint64_t step_index);
 
 /* Split-phase sharded step (configs[3] without an NCCL communicator, e.g. emulated ranks):
- * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, S2_r, 0, V_r[T][4]) per
- * controller (S2 = sum of squared weights, for the ESS diagnostic); mppi_record_size() is the record
- * length in floats per controller (4 + 4T); mppi_get_record_device()
+ * mppi_step_local runs sample..cost and writes this rank's record (m_r, S_r, S2_r, SJ_r, N_r, 0, 0, 0,
+ * V_r[T][4]) per controller (S2 = sum of squared weights, for the ESS diagnostic; SJ / N = sum / count of
+ * the finite costs, for the mean cost); mppi_record_size() is the record length in floats per controller
+ * (8 + 4T); mppi_get_record_device()
  * returns the device pointer of [n_ctrl][record]; mppi_step_finish combines R gathered records
  * (device [R][n_ctrl][record], rank order) into U*. */
 mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step_index);
@@ -156,21 +180,25 @@ int32_t mppi_record_size(const mppi_ctx* ctx);
 const float* mppi_get_record_device(const mppi_ctx* ctx);
 mppi_status mppi_step_finish(mppi_ctx* ctx, const float* d_records, int32_t R);
 
-/* Synchronise and copy the updated U* [n_ctrl][T][4] (and u0 = U*[:,0,:] [n_ctrl][4] if non-NULL) to
- * host. Returns MPPI_ERR_NONFINITE if every J of some controller was non-finite in the last step
- * (that controller's U* is left unchanged). */
+/* Synchronise and copy the updated U* [n_ctrl][T][4] (Eq. 5) and u0 = U*[:,0,:] [n_ctrl][4]
+ * (if non-NULL; "only the first action ... is applied") to host. Returns
+ * MPPI_ERR_NONFINITE if every J of some controller was non-finite in the last step (that controller's U*
+ * is left unchanged); MPPI_ERR_NCCL (context poisoned) if the communicator reports an asynchronous error. */
 mppi_status mppi_get_controls(mppi_ctx* ctx, float* U_out, float* u0_out);
 
-/* Synchronise; out [n_ctrl][4] = (J_min, S = sum w~, ESS = S^2 / sum w~^2, all-nonfinite flag). */
+/* Synchronise; out [n_ctrl][4] = (J_min, S = sum w~, ESS = S^2 / sum w~^2, mean of the finite J; +inf if
+ * none) of the last step (SPEC.md:349 per-step diagnostics). */
 mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out);
 
 /* Test support: copy an internal buffer of the last step to host (synchronises).
  * MPPI_DBG_QUERIES: [n_ctrl][T][K][rps][4] query rows (p_c, |v|) / (p_c + h d, 0), rps = 2 if w_guide != 0
  * MPPI_DBG_SDF:     [n_ctrl][T][K][rps] s per row     MPPI_DBG_COSTS: [n_ctrl][K] J
  * MPPI_DBG_NOISE:   [T][n_ctrl*K][4] standard normals used   MPPI_DBG_TERMS: [n_ctrl][T][K] SDF stage terms
- * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums   MPPI_DBG_RECORD: [n_ctrl][4 + 4T] this rank's record */
+ * MPPI_DBG_PARTIAL: [n_ctrl][K] non-SDF cost sums   MPPI_DBG_RECORD: [n_ctrl][8 + 4T] this rank's record
+ * MPPI_DBG_WEIGHTS: [n_ctrl][K] normalised softmin weights w_k = e^{-(J_k - J_min)/lambda} / S of the last
+ *                   full step (Eq. 5; computed on the device on demand) */
 enum { MPPI_DBG_QUERIES = 0, MPPI_DBG_SDF = 1, MPPI_DBG_COSTS = 2, MPPI_DBG_NOISE = 3, MPPI_DBG_TERMS = 4,
-       MPPI_DBG_PARTIAL = 5, MPPI_DBG_RECORD = 6 };
+       MPPI_DBG_PARTIAL = 5, MPPI_DBG_RECORD = 6, MPPI_DBG_WEIGHTS = 7 };
 mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes);
 
 /* Test support: on != 0 makes every later step also write s per query row (the buffer behind

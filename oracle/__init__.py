@@ -65,6 +65,8 @@ def lib():
         _lib.oracle_rk4_step.argtypes = [P(d), P(d), d, d, d, P(d)]
         _lib.oracle_mlp.argtypes = [P(OracleCfg), P(f), P(f), P(f), P(d)]
         _lib.oracle_mlp.restype = d
+        _lib.oracle_mlp_trace.argtypes = [P(OracleCfg), P(f), P(f), P(f), P(d), P(d)]
+        _lib.oracle_mlp_trace.restype = d
         _lib.oracle_sdf_analytic.argtypes = [d, d, P(d)]
         _lib.oracle_sdf_analytic.restype = d
         _lib.oracle_sdf_rows.argtypes = [P(OracleCfg), P(f), P(f), P(f), P(f), i64, P(d)]
@@ -189,6 +191,17 @@ def mlp(oc: OracleCfg, Ws, bs, z, p) -> float:
     z = _f32(z)
     p = _f64(p)
     return lib().oracle_mlp(C.byref(oc), _p(W, C.c_float), _p(b, C.c_float), _p(z, C.c_float), _p(p, C.c_double))
+
+
+def mlp_trace(oc: OracleCfg, Ws, bs, z, p):
+    """(s, acts [n_hidden][H]): the forward of mlp() with every hidden layer's activations (test support)."""
+    W, b = flat_weights(Ws, bs)
+    z = _f32(z)
+    p = _f64(p)
+    acts = np.zeros((oc.n_hidden, oc.hidden))
+    s = lib().oracle_mlp_trace(C.byref(oc), _p(W, C.c_float), _p(b, C.c_float), _p(z, C.c_float), _p(p, C.c_double),
+                               _p(acts, C.c_double))
+    return s, acts
 
 
 def sdf_analytic(c: float, tana: float, p) -> float:

@@ -232,8 +232,11 @@ void oracle_pe(int bands, const double* p, double* out) {
 }
 
 /* s = g_phi(z, p): layer 1 on [PE(p) | z] (PE(p) = p without PE; full dot, fp64, NOT folded); hidden
- * layers; linear output. W: all layers concatenated, each [out][in] row-major (nn.Linear); b likewise. */
-double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p) {
+ * layers; linear output. W: all layers concatenated, each [out][in] row-major (nn.Linear); b likewise.
+ * acts (may be NULL): [n_hidden][H] post-activation values of every hidden layer, after the bf16
+ * rounding of the quantisation contract (R15) when mlp_bf16 -- test support for the R15 pin. */
+static double mlp_forward(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p,
+                          double* acts) {
     const int L = cfg->latent_dim, H = cfg->hidden;
     double* a = (double*)malloc(sizeof(double) * (size_t)H);
     double* an = (double*)malloc(sizeof(double) * (size_t)H);
@@ -251,6 +254,7 @@ double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const f
         double v = act_fn(cfg->activation, acc);
         a[i] = cfg->mlp_bf16 ? bf16_round(v) : v;
     }
+    if (acts) memcpy(acts, a, sizeof(double) * (size_t)H);
     Wl += (size_t)H * in1;
     bl += H;
     for (int l = 1; l < cfg->n_hidden; ++l) {
@@ -266,6 +270,7 @@ double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const f
             an[i] = cfg->mlp_bf16 ? bf16_round(v) : v;
         }
         memcpy(a, an, sizeof(double) * (size_t)H);
+        if (acts) memcpy(acts + (size_t)l * H, a, sizeof(double) * (size_t)H);
         Wl += (size_t)H * H;
         bl += H;
     }
@@ -279,6 +284,16 @@ double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const f
     free(a);
     free(an);
     return s;
+}
+
+double oracle_mlp(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p) {
+    return mlp_forward(cfg, W, b, z, p, NULL);
+}
+
+/* The same forward, also returning every hidden layer's activations acts [n_hidden][H] (test support). */
+double oracle_mlp_trace(const oracle_cfg* cfg, const float* W, const float* b, const float* z, const double* p,
+                        double* acts) {
+    return mlp_forward(cfg, W, b, z, p, acts);
 }
 
 /* Eq. 1-2: r(p) = max(|y|,|z|); s_guide = c + |x| tan(alpha) - r(p). */

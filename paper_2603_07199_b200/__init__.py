@@ -33,7 +33,7 @@ class Controller:
 
     def __init__(self, cfg, *, device: int = 0, stream=None, noise_mode: str = "device", world_size: int = 1,
                  rank: int = 0, K_global: int | None = None, k_offset: int = 0, nccl_id: bytes | None = None,
-                 seed: int | None = None, debug_outputs: bool = False):
+                 seed: int | None = None, debug_outputs: bool = False, ctrl_offset: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2603_07199_b200.Controller needs a CUDA device (no CPU fallback)")
@@ -46,7 +46,7 @@ class Controller:
         self.stream = stream
         self.c = make_config(cfg, device=device, stream=stream.cuda_stream, noise_mode=noise_mode,
                              world_size=world_size, rank=rank, K_global=K_global, k_offset=k_offset,
-                             nccl_id=nccl_id, seed=seed)
+                             nccl_id=nccl_id, seed=seed, ctrl_offset=ctrl_offset)
         nbytes = self.lib.mppi_workspace_bytes(C.byref(self.c))
         if nbytes == 0:
             raise MppiError(-1, self.lib.mppi_last_error().decode())
@@ -92,6 +92,23 @@ class Controller:
         z = _f32(z)
         T_q = _f32(T_q)
         _lib._check(self.lib.mppi_set_latent(self.ctx, ctrl, _lib._ptr(z), _lib._ptr(T_q)))
+
+    def set_latent_frame(self, z, T_q, t_frame: float, valid: bool = True, ctrl: int = -1):
+        """A depth frame for the latent cache: valid frames refresh (z, T_q) and record
+        t_frame; invalid (occluded) frames keep the cached pair (z, T_q may be None)."""
+        zp = tp = None
+        if valid:
+            z, T_q = _f32(z), _f32(T_q)
+            zp, tp = _lib._ptr(z), _lib._ptr(T_q)
+        _lib._check(self.lib.mppi_set_latent_frame(self.ctx, ctrl, zp, tp, float(t_frame), 1 if valid else 0))
+
+    def latent_status(self):
+        """(t_frame [n], steps since the cached frame [n], invalid frames since [n])."""
+        t = np.zeros(self.n, np.float64)
+        st = np.zeros(self.n, np.int64)
+        inv = np.zeros(self.n, np.int64)
+        _lib._check(self.lib.mppi_get_latent_status(self.ctx, _lib._ptr(t), _lib._ptr(st), _lib._ptr(inv)))
+        return t, st, inv
 
     def set_nominal(self, U, ctrl: int = -1):
         U = _f32(U)
@@ -155,7 +172,7 @@ class Controller:
     def debug(self, what: str) -> np.ndarray:
         n, K, T, r = self.n, self.K, self.T, self.rps
         shapes = {"queries": (n, T, K, r, 4), "sdf": (n, T, K, r), "costs": (n, K), "noise": (T, n * K, 4),
-                  "terms": (n, T, K), "partial": (n, K), "record": (n, 4 + 4 * T)}
+                  "terms": (n, T, K), "partial": (n, K), "record": (n, _lib.REC_HEAD + 4 * T), "weights": (n, K)}
         out = np.zeros(shapes[what], np.float32)
         _lib._check(self.lib.mppi_debug_copy(self.ctx, DBG[what], _lib._ptr(out), out.nbytes))
         return out

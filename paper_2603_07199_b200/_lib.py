@@ -11,15 +11,16 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmppi_b200.so")
 
-MPPI_ABI_VERSION = 2
+MPPI_ABI_VERSION = 3
+REC_HEAD = 8   # softmin record header floats (m, S, S2, SJ, N, 0, 0, 0), then V[T][4]
 STATUS = {0: "OK", -1: "INVALID", -2: "CUDA", -3: "NCCL", -4: "NOT_READY", -5: "NONFINITE", -6: "OOM",
           -7: "POISONED", -8: "UNSUPPORTED"}
 MPPI_OK, MPPI_ERR_INVALID, MPPI_ERR_NONFINITE, MPPI_ERR_UNSUPPORTED = 0, -1, -5, -8
-DBG = {"queries": 0, "sdf": 1, "costs": 2, "noise": 3, "terms": 4, "partial": 5, "record": 6}
+DBG = {"queries": 0, "sdf": 1, "costs": 2, "noise": 3, "terms": 4, "partial": 5, "record": 6, "weights": 7}
 
 # every symbol include/mppi.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["mppi_workspace_bytes", "mppi_create", "mppi_destroy", "mppi_get_nccl_unique_id",
-           "mppi_set_sdf_weights", "mppi_set_latent", "mppi_set_nominal", "mppi_set_noise", "mppi_step",
+           "mppi_set_sdf_weights", "mppi_set_latent", "mppi_set_latent_frame", "mppi_get_latent_status", "mppi_set_nominal", "mppi_set_noise", "mppi_step",
            "mppi_step_device", "mppi_step_local", "mppi_record_size", "mppi_get_record_device",
            "mppi_step_finish", "mppi_get_controls", "mppi_get_diagnostics", "mppi_debug_copy", "mppi_sdf_eval",
            "mppi_set_profiling", "mppi_set_debug_outputs", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_debug_trace",
@@ -50,6 +51,8 @@ class MppiConfig(C.Structure):
         ("q_gate", C.c_float), ("q_vis", C.c_float), ("q_sdf", C.c_float), ("d_safe", C.c_float),
         ("sdf_provider", C.c_int32), ("gate_c", C.c_float), ("gate_tana", C.c_float),
         ("pe_bands", C.c_int32),
+        # ABI 3
+        ("ctrl_offset", C.c_int64),
     ]
 
 
@@ -74,6 +77,8 @@ def load(path: str | None = None):
         "mppi_get_nccl_unique_id": ([vp], i32),
         "mppi_set_sdf_weights": ([vp, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(vp), C.POINTER(vp)], i32),
         "mppi_set_latent": ([vp, i32, vp, vp], i32),
+        "mppi_set_latent_frame": ([vp, i32, vp, vp, C.c_double, i32], i32),
+        "mppi_get_latent_status": ([vp, vp, vp, vp], i32),
         "mppi_set_nominal": ([vp, i32, vp], i32),
         "mppi_set_noise": ([vp, vp], i32),
         "mppi_step": ([vp, vp, vp, u64], i32),
@@ -112,7 +117,7 @@ def _ptr(a: np.ndarray):
 
 def make_config(cfg, *, device: int = 0, stream: int = 0, noise_mode: str = "device", world_size: int = 1,
                 rank: int = 0, K_global: int | None = None, k_offset: int = 0, nccl_id: bytes | None = None,
-                seed: int | None = None) -> MppiConfig:
+                seed: int | None = None, ctrl_offset: int = 0) -> MppiConfig:
     """Fill the C config from any object with the synth.MPPIConfig attribute names."""
     c = MppiConfig()
     c.abi_version = MPPI_ABI_VERSION
@@ -144,4 +149,5 @@ def make_config(cfg, *, device: int = 0, stream: int = 0, noise_mode: str = "dev
     c.sdf_provider = getattr(cfg, "sdf_provider", 0)
     c.gate_c, c.gate_tana = getattr(cfg, "gate_c", 0.5), getattr(cfg, "gate_tana", 0.0)
     c.pe_bands = getattr(cfg, "pe_bands", 0)
+    c.ctrl_offset = ctrl_offset
     return c

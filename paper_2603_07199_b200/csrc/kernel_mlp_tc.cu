@@ -37,6 +37,7 @@
 
 #include "../../include/mppi.h"
 #include "mppi_internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace mppi {
 namespace tc {
@@ -82,259 +83,6 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #define MPPI_L1_SMEM 1
 #endif
 constexpr int kTileRows = 128;
-
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-// Arrive on a barrier given by its shared::cluster address (possibly in the peer CTA). Default
-// (.release.cta) semantics: the only data ordered through these barriers are TMEM accesses, which the
-// tcgen05.fence::before/after_thread_sync pair orders; a .cluster-scope release fence costs ~1k cycles.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
-    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-template <bool kCluster>
-__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    return ok != 0;
-}
-// Non-blocking probe of a phase.
-__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    return ok != 0;
-}
-#ifndef MPPI_ISSUER_HINT_NS
-#define MPPI_ISSUER_HINT_NS 100
-#endif
-// Issuer-side wait: try_wait with a 100 ns suspend-time hint (measured 3% faster than the default hint
-// at configs[2]; MPPI_ISSUER_SPIN: spin on test_wait).
-__device__ __forceinline__ void mbar_wait_issuer(uint32_t a, uint32_t parity) {
-    uint32_t n = 0;
-#if defined(MPPI_ISSUER_SPIN)
-    while (!mbar_test(a, parity))
-        if (++n > (1u << 28)) __trap();
-#else
-    for (;;) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-            "selp.b32 %0, 1, 0, P1;\n\t}"
-            : "=r"(ok) : "r"(a), "r"(parity), "n"(MPPI_ISSUER_HINT_NS) : "memory");
-        if (ok) break;
-        if (++n > (1u << 26)) __trap();
-    }
-#endif
-}
-// Bounded wait: a schedule bug traps (launch error) instead of hanging the GPU.
-template <bool kCluster = false>
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t n = 0;
-    while (!mbar_try_wait<kCluster>(bar, parity)) {
-        if (++n > (1u << 22)) __trap();
-    }
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-// One lane of a converged warp (elect.sync): the warp runs the issue loop with warp-uniform values,
-// so the MMA operands stay in uniform registers (no per-MMA R2UR waterfall loop)
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
-    return pred != 0;
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-template <int CG>
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-    if constexpr (CG == 1) {
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-    } else {   // arrive on the barrier at the same offset in both CTAs of the pair
-        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                         bar), "h"((uint16_t)3)
-                     : "memory");
-    }
-}
-// D[tmem] (+)= A[tmem] x B[smem]^T  (bf16 in, fp32 accumulate; M, N from idesc; K = 16)
-template <int CG>
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    if constexpr (CG == 1) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    }
-}
-// D[tmem] (+)= A[smem] x B[smem]^T
-template <int CG>
-__device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    if constexpr (CG == 1) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// wait::ld tied to the registers of the load it completes, so no use of them can be scheduled above it
-__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[16]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-                 :
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart (SBO).
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// UMMA shared-memory descriptor: K-major, no swizzle (8-row x 16-byte core matrices), K = 16 operand:
-// the two K cores of a row group 128 B apart (LBO), 8-row groups 256 B apart (SBO).
-__device__ __forceinline__ uint64_t smem_desc_kmajor_noswz(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
-           ((uint64_t)1 << 46);
-}
-// Instruction descriptor kind::f16: D fp32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ float tanh_approx(float x) {
-    float y;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-// Two IEEE fp32 FMAs in one FFMA2 instruction (sm_100): lane-wise a * b + c, bitwise equal to fmaf.
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    float2 r;
-    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(r.x), "=f"(r.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return r;
-}
-// Biases (and, for layer 1, the position weights and folded bias) are stored pre-scaled by
-// kPre<ACT> so that SiLU needs one FFMA to form h = x/2: silu(x) = x sigmoid(x) = h + h tanh(h).
-template <int ACT>
-constexpr float kPre = ACT == MPPI_ACT_SILU ? 0.5f : 1.0f;
-// pre = acc * kPre + b_scaled (GEMM epilogue) or the layer-1 dot with scaled weights
-template <int ACT>
-__device__ __forceinline__ float act_pre(float pre) {
-    if constexpr (ACT == MPPI_ACT_RELU) {
-        return fmaxf(pre, 0.f);
-    } else if constexpr (ACT == MPPI_ACT_SILU) {
-        return fmaf(pre, tanh_approx(pre), pre);
-    } else {
-        return fmaxf(pre, 0.f) + log1pf(__expf(-fabsf(pre)));
-    }
-}
-
-// bf16x2 of act(x0) (low half) and act(x1) (high half); ReLU is fused into the conversion
-// (cvt.rn.relu: relu(rne(x)) = rne(relu(x)), the sign survives rounding).
-template <int ACT>
-__device__ __forceinline__ uint32_t act_pack(float x0, float x1) {
-    if constexpr (ACT == MPPI_ACT_RELU) {
-        uint32_t r;
-        asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x1), "f"(x0));
-        return r;
-    } else if constexpr (ACT == MPPI_ACT_SILU) {   // h + h tanh(h) for both halves in one FFMA2
-        const float2 h = make_float2(x0, x1);
-        const float2 s = ffma2(h, make_float2(tanh_approx(x0), tanh_approx(x1)), h);
-        return pack_bf16x2(s.x, s.y);
-    } else {
-        return pack_bf16x2(act_pre<ACT>(x0), act_pre<ACT>(x1));
-    }
-}
 
 // ------------------------------------------------------------------ configuration
 template <int H, int G, int PEB = 0>
@@ -883,8 +631,11 @@ template <int H, int G, int ACT, int PEB>
 cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s) {
     using C = Cfg<H, G, PEB>;
-    static bool attr_set = false;
-    static int max_groups = 0;   // co-resident CTA groups (clusters) on this device: the persistent grid
+    // per device (a process may drive several): the dynamic-smem opt-in and the persistent grid size
+    constexpr int kMaxDev = 64;
+    static int max_groups[kMaxDev] = {};   // co-resident CTA groups (clusters) on the device; 0 = not set up
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -896,28 +647,28 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (!attr_set) {
+    if (max_groups[dev] == 0) {
         cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT, PEB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
-        int dev, n_sm = 0;
-        cudaGetDevice(&dev);
+        int n_sm = 0;
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        max_groups = n_sm / C::CG;
+        int groups = n_sm / C::CG;
         // with clusters, GPC/TPC floor-sweeping can leave fewer pairs co-resident than SMs/2: a static
         // round-robin over more groups than fit would serialise a second wave
         int clusters = 0;
-        cfg.gridDim = dim3((unsigned)(max_groups * C::CG));
+        cfg.gridDim = dim3((unsigned)(groups * C::CG));
         if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT, PEB>, &cfg) == cudaSuccess && clusters > 0)
-            max_groups = clusters < max_groups ? clusters : max_groups;
+            groups = clusters < groups ? clusters : groups;
         cudaGetLastError();
-        attr_set = true;
+        if (groups < 1) return cudaErrorInvalidConfiguration;
+        max_groups[dev] = groups;
         if (getenv("MPPI_VERBOSE"))
-            fprintf(stderr, "[mppi] k_mlp_tc<%d,%d,%d>: %d SMs, %d co-resident groups of %d CTAs, smem %d B\n", H, G, ACT,
-                    n_sm, max_groups, C::CG, C::SMEM);
+            fprintf(stderr, "[mppi] k_mlp_tc<%d,%d,%d> dev %d: %d SMs, %d co-resident groups of %d CTAs, smem %d B\n", H, G,
+                    ACT, dev, n_sm, groups, C::CG, C::SMEM);
     }
     const long long tiles = (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
     if (tiles == 0) return cudaSuccess;
-    const long long groups = tiles < max_groups ? tiles : max_groups;
+    const long long groups = tiles < max_groups[dev] ? tiles : max_groups[dev];
     cfg.gridDim = dim3((unsigned)(groups * C::CG));
     return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
                               (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,

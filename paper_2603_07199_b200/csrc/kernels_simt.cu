@@ -55,11 +55,19 @@ __device__ __forceinline__ float4 philox_normals(unsigned long long g, int t, un
     return make_float4(-r0 * c0, -r0 * s0, -r1 * c1, -r1 * s1);
 }
 
+// Global sample index keying the noise (reading R24'): controller ctrl_offset + b of the whole job, sample
+// k_offset + k of its K_global, so every sharding (samples over ranks, configs[3]; controllers over ranks,
+// configs[4]) draws exactly the samples of the unsharded job.
+__device__ __forceinline__ unsigned long long global_sample(const Params& p, int bb, int k) {
+    return (unsigned long long)(p.ctrl_offset + bb) * (unsigned long long)p.K_global + (unsigned long long)p.k_offset +
+           (unsigned long long)k;
+}
+
 // ------------------------------------------------------------------ K0: noise + warm-start shift
 // (debug / standalone form; the step graph fuses both into k_rollout)
 // Thread i < n_ctrl*T: U_nom[b][t] = U_out[b][min(t + (step>0), T-1)] (PAPER.md:144 shift).
 // Thread i < T*n_ctrl*K (gen): Philox4x32-10(key = seed, ctr = (g, t, step_lo, step_hi)), g = global
-// sample index b*K_global + k_offset + k; u = ((x >> 9) + 0.5) 2^-23; Box-Muller -> 4 normals.
+// sample index global_sample(b, k); u = ((x >> 9) + 0.5) 2^-23; Box-Muller -> 4 normals.
 __global__ void __launch_bounds__(256) k_noise_shift(Params p, Buffers b, int gen) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long step = *b.step;
@@ -73,7 +81,7 @@ __global__ void __launch_bounds__(256) k_noise_shift(Params p, Buffers b, int ge
         const int t = (int)(i / NK);
         const long long j = i - (long long)t * NK;
         const int bb = (int)(j / p.K), k = (int)(j - (long long)bb * p.K);
-        const unsigned long long g = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+        const unsigned long long g = global_sample(p, bb, k);
         b.noise[i] = philox_normals(g, t, step, p.seed);
     }
 }
@@ -112,7 +120,7 @@ __device__ void rollout_noise_producer(const Params& p, const Buffers& b, int bb
                                        unsigned long long step, float4 (*s_n)[kRolloutBlock]) {
     const bool valid = k < p.K;
     const long long NK = (long long)p.n_ctrl * p.K, col = (long long)bb * p.K + k;
-    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+    const unsigned long long gidx = global_sample(p, bb, k);
     if (valid) {
         const float4 n = philox_normals(gidx, 0, step, p.seed);
         s_n[0][lt] = n;
@@ -168,7 +176,7 @@ __global__ void __launch_bounds__(2 * kRolloutBlock) k_rollout(Params p, Buffers
     const float4* Uo = reinterpret_cast<const float4*>(b.U_out) + (long long)bb * p.T;
     const long long NK = (long long)p.n_ctrl * p.K;
     const long long col = (long long)bb * p.K + k;
-    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+    const unsigned long long gidx = global_sample(p, bb, k);
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity, inv_mass = 1.f / p.mass;
     float part = 0.f;
     // software pipelining: the noise / nominal of step t+1 are produced while step t integrates
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(2 * kRolloutBlock) k_rollout_paper(Params p, B
     auto nominal = [&](int t) { return t < kMaxTStaged ? s_U[t] : Uo[min(t + sh, p.T - 1)]; };
     const long long NK = (long long)p.n_ctrl * p.K;
     const long long col = (long long)bb * p.K + k;
-    const unsigned long long gidx = (unsigned long long)bb * p.K_global + (unsigned long long)p.k_offset + k;
+    const unsigned long long gidx = global_sample(p, bb, k);
     const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f;
     float part = 0.f;
     float4 n_next = DEV ? make_float4(0.f, 0.f, 0.f, 0.f) : b.noise[col];
@@ -451,7 +459,8 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 //   J_k = partial_k + sum_t term[t][k] (non-finite -> +inf)                         PAPER.md:185 (Eq. 10)
 //   m_b = min_k J_k; w_k = exp((m_b - J_k)/lambda); S_b = sum w; S2_b = sum w^2;
 //   V_b[t] = sum_k w_k (clamp(U*_t + sigma n_{t,k}) - U*_t)   (clamped samples, reading R5)
-// -> block record (m_b, S_b, S2_b, V_b). The last block of the controller (atomic ticket) combines the
+// -> block record (m_b, S_b, S2_b, SJ_b, N_b, 0, 0, 0, V_b) with SJ_b / N_b the sum / count of the finite J
+// (mean-cost diagnostic). The last block of the controller (atomic ticket) combines the
 // records in block order: m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b,
 // U* <- U* + V/S (Eq. 5) -- the shard-combine identity, so the result is deterministic.
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
@@ -487,7 +496,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     const int bb = blockIdx.y, nblk = gridDim.x, tz = blockIdx.z, nz_t = gridDim.z;
     const int kk = threadIdx.x % kSoftminBlock, half = threadIdx.x / kSoftminBlock;
     const int k = blockIdx.x * kSoftminBlock + kk;
-    const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
+    const int W = kRecHead + 4 * p.T;   // m, S, S2, SJ, N, pad x3, V[T][4] (16-B aligned)
     // ---- phase 1: two threads per sample, each summing half of the horizon's terms in t order
     float J = INFINITY;
     {
@@ -520,7 +529,14 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     const float S = block_reduce(w, red, false);
     const float S2 = block_reduce(w * w, red, false);
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
-    if (threadIdx.x == 0 && tz == 0) { rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = 0.f; }
+    if (tz == 0) {   // mean-cost diagnostic: sum and count of the finite costs
+        const float SJ = block_reduce(J < INFINITY ? J : 0.f, red, false);
+        const float NJ = block_reduce(J < INFINITY ? 1.f : 0.f, red, false);
+        if (threadIdx.x == 0) {
+            rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = SJ;
+            rec[4] = NJ; rec[5] = rec[6] = rec[7] = 0.f;
+        }
+    }
     // ---- phase 2: warp per time step (coalesced over the block's samples), fixed shuffle tree
     const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
     const long long NK = (long long)p.n_ctrl * p.K;
@@ -560,7 +576,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
             v2 += __shfl_xor_sync(0xFFFFFFFFu, v2, o);
             v3 += __shfl_xor_sync(0xFFFFFFFFu, v3, o);
         }
-        if (lane == 0) reinterpret_cast<float4*>(rec + 4)[t] = make_float4(v0, v1, v2, v3);
+        if (lane == 0) reinterpret_cast<float4*>(rec + kRecHead)[t] = make_float4(v0, v1, v2, v3);
     }
     // ---- last block of this controller combines the block records in order
     __threadfence();
@@ -576,7 +592,7 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     for (int i = threadIdx.x; i < nblk; i += blockDim.x) mi_loc = fminf(mi_loc, __ldcg(recs + (long long)i * W));
     const float mg = block_reduce(mi_loc, red, true);
     const bool ok = mg < INFINITY;
-    float sl = 0.f, s2l = 0.f;
+    float sl = 0.f, s2l = 0.f, sjl = 0.f, njl = 0.f;
     for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
         const float* r = recs + (long long)i * W;
         const float mi = __ldcg(r);
@@ -584,9 +600,13 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
         if (i < kSoftminThreads) s_f[i] = f;
         sl += __ldcg(r + 1) * f;
         s2l += __ldcg(r + 2) * f * f;
+        sjl += __ldcg(r + 3);
+        njl += __ldcg(r + 4);
     }
     const float Sg = block_reduce(sl, red, false);
     const float S2g = block_reduce(s2l, red, false);
+    const float SJg = block_reduce(sjl, red, false);
+    const float NJg = block_reduce(njl, red, false);
     for (int tc = threadIdx.x; tc < 4 * p.T; tc += blockDim.x) {
         float V = 0.f;
         if (ok) {
@@ -594,12 +614,12 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
             for (int i = 0; i < nblk; ++i) {
                 const float f = i < kSoftminThreads ? s_f[i]
                                                   : expf((mg - __ldcg(recs + (long long)i * W)) * p.inv_lambda);
-                V = fmaf(__ldcg(recs + (long long)i * W + 4 + tc), f, V);
+                V = fmaf(__ldcg(recs + (long long)i * W + kRecHead + tc), f, V);
             }
         }
         const int t = tc >> 2, c = tc & 3;
         if (write_record) {
-            b.record[(long long)bb * W + 4 + tc] = V;
+            b.record[(long long)bb * W + kRecHead + tc] = V;
         } else {
             const float Uv = b.U_nom[((long long)bb * p.T + t) * 4 + c];
             b.U_out[((long long)bb * p.T + t) * 4 + c] = (ok && Sg > 0.f) ? Uv + V / Sg : Uv;
@@ -608,13 +628,14 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     if (threadIdx.x == 0) {
         if (write_record) {
             float* out = b.record + (long long)bb * W;
-            out[0] = mg; out[1] = Sg; out[2] = S2g; out[3] = 0.f;
+            out[0] = mg; out[1] = Sg; out[2] = S2g; out[3] = SJg;
+            out[4] = NJg; out[5] = out[6] = out[7] = 0.f;
         } else {
             float* d = b.diag + bb * 4;
             d[0] = mg;
             d[1] = Sg;
             d[2] = S2g > 0.f ? Sg * Sg / S2g : 0.f;
-            d[3] = ok ? 0.f : 1.f;
+            d[3] = NJg > 0.f ? SJg / NJg : INFINITY;
             b.flags[bb] = ok ? 0 : 1;
         }
         b.tickets[bb] = 0u;   // ready for the next step (kernel boundary orders it)
@@ -641,12 +662,17 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n_ctrl * p.T) return;
     const int bb = i / p.T, t = i % p.T;
-    const int W = 4 + 4 * p.T;   // m, S, S2, pad, V[T][4] (16-B aligned)
+    const int W = kRecHead + 4 * p.T;   // m, S, S2, SJ, N, pad x3, V[T][4] (16-B aligned)
     float m = INFINITY;
     for (int r = 0; r < R; ++r) m = fminf(m, recs[((long long)r * p.n_ctrl + bb) * W]);
     const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
     float4 Un = U;
-    float S = 0.f, S2 = 0.f, v[4] = {0.f, 0.f, 0.f, 0.f};
+    float S = 0.f, S2 = 0.f, SJ = 0.f, NJ = 0.f, v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < R; ++r) {
+        const float* rec = recs + ((long long)r * p.n_ctrl + bb) * W;
+        SJ += rec[3];
+        NJ += rec[4];
+    }
     if (isfinite(m)) {
         for (int r = 0; r < R; ++r) {
             const float* rec = recs + ((long long)r * p.n_ctrl + bb) * W;
@@ -654,7 +680,7 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
             const float f = expf((m - rec[0]) * p.inv_lambda);
             S += rec[1] * f;
             S2 += rec[2] * f * f;
-            for (int c = 0; c < 4; ++c) v[c] += rec[4 + 4 * t + c] * f;
+            for (int c = 0; c < 4; ++c) v[c] += rec[kRecHead + 4 * t + c] * f;
         }
         if (S > 0.f) {
             Un.x = U.x + v[0] / S; Un.y = U.y + v[1] / S; Un.z = U.z + v[2] / S; Un.w = U.w + v[3] / S;
@@ -666,7 +692,7 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
         d[0] = m;
         d[1] = S;
         d[2] = S2 > 0.f ? S * S / S2 : 0.f;
-        d[3] = isfinite(m) ? 0.f : 1.f;
+        d[3] = NJ > 0.f ? SJ / NJ : INFINITY;
         b.flags[bb] = isfinite(m) ? 0 : 1;
     }
 }
@@ -674,6 +700,22 @@ __global__ void k_combine(Params p, Buffers b, const float* recs, int R) {
 void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s) {
     const int n = p.n_ctrl * p.T;
     k_combine<<<(n + 127) / 128, 128, 0, s>>>(p, b, recs, R);
+}
+
+// ------------------------------------------------------------------ debug: normalised softmin weights
+// w_k = exp(-(J_k - J_min)/lambda) / S (Eq. 5) of the last step, from its costs and the
+// (J_min, S) the update used (diag); on demand for mppi_debug_copy(MPPI_DBG_WEIGHTS), not on the step path.
+__global__ void k_weights(Params p, Buffers b) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)p.n_ctrl * p.K) return;
+    const int bb = (int)(i / p.K);
+    const float m = b.diag[bb * 4], S = b.diag[bb * 4 + 1], J = b.J[i];
+    b.weights[i] = (J < INFINITY && m < INFINITY && S > 0.f) ? expf((m - J) * p.inv_lambda) / S : 0.f;
+}
+
+void launch_weights(const Params& p, const Buffers& b, cudaStream_t s) {
+    const long long n = (long long)p.n_ctrl * p.K;
+    k_weights<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, b);
 }
 
 // ------------------------------------------------------------------ analytic Gate-SDF provider (F4)

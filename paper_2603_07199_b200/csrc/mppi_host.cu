@@ -33,7 +33,8 @@ struct Layout {
 
 enum BufId {
     B_W1P, B_W1PE, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
-    B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_TICK, B_BLKREC, B_REC, B_GATH, B_DIAG, B_FLAGS, B_COUNT
+    B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_TICK, B_BLKREC, B_REC, B_GATH, B_DIAG, B_FLAGS, B_WGT,
+    B_COUNT
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -43,7 +44,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     const size_t Ld = (size_t)c->latent_dim, G = (size_t)(c->n_hidden - 1);
     const size_t rps = c->w_guide != 0.f ? 2 : 1;
     const size_t world = (size_t)(c->world_size > 0 ? c->world_size : 1);
-    const size_t recw = 4 + 4 * T;
+    const size_t recw = kRecHead + 4 * T;
     size_t sz[B_COUNT];
     sz[B_W1P] = 16 * H;
     sz[B_W1PE] = 4 * H * (size_t)(3 + 6 * c->pe_bands);
@@ -74,6 +75,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_GATH] = 4 * world * n * recw;
     sz[B_DIAG] = 16 * n;
     sz[B_FLAGS] = 4 * n;
+    sz[B_WGT] = 4 * n * K;
     size_t o = 0;
     for (int i = 0; i < B_COUNT; ++i) {
         o = align_up(o, 1024);
@@ -125,7 +127,23 @@ struct mppi_ctx {
     cudaEvent_t prof_ev[kNumStages + 1] = {};
     bool prof_valid = false;
     ncclComm_t comm = nullptr;
+    ncclResult_t nccl_err = ncclSuccess;   // last NCCL call's result inside the step capture
     int last_mode = -1;
+    // latent cache status per controller: frame time, steps and invalid frames since
+    std::vector<double> latent_t;
+    std::vector<int64_t> latent_steps, latent_invalid;
+};
+
+// Every entry point that touches the device runs on the context's device and restores the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
 };
 
 #define CUDA_TRY(ctx, expr)                                                                             \
@@ -154,6 +172,7 @@ static mppi_status validate(const mppi_config* c) {
     if (c->n_ctrl < 1 || c->K < 1 || c->T < 1) return fail(MPPI_ERR_INVALID, "n_ctrl, K, T must be >= 1");
     if (c->K_global < c->K) return fail(MPPI_ERR_INVALID, "K_global < K");
     if (c->k_offset < 0 || c->k_offset + c->K > c->K_global) return fail(MPPI_ERR_INVALID, "k_offset out of range");
+    if (c->ctrl_offset < 0) return fail(MPPI_ERR_INVALID, "ctrl_offset < 0");
     if (!(c->dt > 0.f) || !(c->lambda > 0.f) || !(c->mass > 0.f)) return fail(MPPI_ERR_INVALID, "dt, lambda, mass > 0");
     if (!(c->sdf_scale > 0.f)) return fail(MPPI_ERR_INVALID, "sdf_scale > 0");
     if (c->w_guide != 0.f && !(c->fd_h > 0.f)) return fail(MPPI_ERR_INVALID, "fd_h > 0 with guidance");
@@ -225,8 +244,13 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     ctx->cfg = *cfg;
     ctx->lay = L;
     ctx->stream = (cudaStream_t)cfg->stream;
-    cudaError_t e = cudaSetDevice(cfg->device);
-    if (e != cudaSuccess) { delete ctx; return fail(MPPI_ERR_CUDA, cudaGetErrorString(e)); }
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || cfg->device < 0 || cfg->device >= n_dev) {
+        delete ctx;
+        return fail(MPPI_ERR_INVALID, "cfg.device is not a CUDA device of this process");
+    }
+    DeviceGuard dg(cfg->device);
+    cudaError_t e;
     if (!d_ws) {
         e = cudaMalloc(&ctx->ws, L.total);
         if (e != cudaSuccess) { delete ctx; return fail(MPPI_ERR_OOM, cudaGetErrorString(e)); }
@@ -266,12 +290,13 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     b.gathered = (float*)(base + L.off[B_GATH]);
     b.diag = (float*)(base + L.off[B_DIAG]);
     b.flags = (int*)(base + L.off[B_FLAGS]);
+    b.weights = (float*)(base + L.off[B_WGT]);
 
     Params& p = ctx->p;
     p.n_ctrl = cfg->n_ctrl; p.K = cfg->K; p.T = cfg->T;
     p.rps = cfg->w_guide != 0.f ? 2 : 1;
     p.H = cfg->hidden; p.L = cfg->latent_dim; p.n_gemm = cfg->n_hidden - 1; p.act = cfg->activation;
-    p.K_global = cfg->K_global; p.k_offset = cfg->k_offset;
+    p.K_global = cfg->K_global; p.k_offset = cfg->k_offset; p.ctrl_offset = cfg->ctrl_offset;
     p.dt = cfg->dt; p.inv_lambda = 1.f / cfg->lambda; p.mass = cfg->mass; p.gravity = cfg->gravity;
     for (int i = 0; i < 4; ++i) { p.u_lo[i] = cfg->u_lo[i]; p.u_hi[i] = cfg->u_hi[i]; p.sigma[i] = cfg->sigma[i]; }
     p.w_goal = cfg->w_goal; p.w_sdf = cfg->w_sdf; p.inv_sdf_scale = 1.f / cfg->sdf_scale;
@@ -289,6 +314,9 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.pe_bands = cfg->pe_bands;
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
     ctx->latent_set.assign(cfg->n_ctrl, 0);
+    ctx->latent_t.assign(cfg->n_ctrl, NAN);
+    ctx->latent_steps.assign(cfg->n_ctrl, 0);
+    ctx->latent_invalid.assign(cfg->n_ctrl, 0);
 
     auto cleanup = [&](mppi_status s, const std::string& m) {
         mppi_destroy(ctx);
@@ -328,6 +356,11 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
 
 mppi_status mppi_destroy(mppi_ctx* ctx) {
     if (!ctx) return MPPI_OK;
+    DeviceGuard dg(ctx->cfg.device);
+    // a step may still be in flight: nothing is released before the context's work has drained
+    if (ctx->work) cudaStreamSynchronize(ctx->work);
+    if (ctx->stream || ctx->work) cudaStreamSynchronize(ctx->stream);
+    cudaGetLastError();
     for (auto& g : ctx->graph)
         if (g) cudaGraphExecDestroy(g);
     for (int i = 0; i < kStaging; ++i) {
@@ -337,7 +370,7 @@ mppi_status mppi_destroy(mppi_ctx* ctx) {
     for (auto& e : ctx->prof_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
-    if (ctx->work) { cudaStreamSynchronize(ctx->work); cudaStreamDestroy(ctx->work); }
+    if (ctx->work) cudaStreamDestroy(ctx->work);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->own_ws && ctx->ws) cudaFree(ctx->ws);
@@ -350,6 +383,10 @@ mppi_status mppi_destroy(mppi_ctx* ctx) {
         if (!(ctx)) return fail(MPPI_ERR_INVALID, "ctx is NULL");             \
         if ((ctx)->poisoned) return fail(MPPI_ERR_POISONED, "context poisoned by an earlier CUDA/NCCL error"); \
     } while (0)
+// CHECK_CTX + run the rest of the entry point on the context's device
+#define ENTER_CTX(ctx)                       \
+    CHECK_CTX(ctx);                          \
+    DeviceGuard _dev_guard((ctx)->cfg.device)
 
 static void invalidate_graphs(mppi_ctx* ctx) {
     for (auto& g : ctx->graph)
@@ -358,7 +395,7 @@ static void invalidate_graphs(mppi_ctx* ctx) {
 
 mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t* in_dim, const int32_t* out_dim,
                                  const float* const* W, const float* const* bvec) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     const mppi_config& c = ctx->cfg;
     const int H = c.hidden, Ld = c.latent_dim, G = c.n_hidden - 1;
     if (n_layers != c.n_hidden + 1 || !in_dim || !out_dim || !W || !bvec)
@@ -410,15 +447,23 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     return MPPI_OK;
 }
 
-mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q) {
-    CHECK_CTX(ctx);
+static mppi_status set_latent_impl(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q, double t_frame,
+                                   int32_t valid) {
+    ENTER_CTX(ctx);
     const mppi_config& c = ctx->cfg;
     const bool gate = c.sdf_provider == MPPI_SDF_GATE;
-    if (!ctx->weights && !gate) return fail(MPPI_ERR_NOT_READY, "set weights before latents");
-    if (ctrl < -1 || ctrl >= c.n_ctrl || (!z && c.latent_dim > 0) || !T_q) return fail(MPPI_ERR_INVALID, "bad ctrl / NULL");
+    if (ctrl < -1 || ctrl >= c.n_ctrl) return fail(MPPI_ERR_INVALID, "bad ctrl");
     const int c0 = ctrl < 0 ? 0 : ctrl, cnt = ctrl < 0 ? c.n_ctrl : 1;
+    if (!valid) {   // occluded / invalid frame: the cached (z, T_q) stays in use
+        for (int i = 0; i < cnt; ++i) ++ctx->latent_invalid[c0 + i];
+        return MPPI_OK;
+    }
+    if (!ctx->weights && !gate) return fail(MPPI_ERR_NOT_READY, "set weights before latents");
+    if ((!z && c.latent_dim > 0) || !T_q) return fail(MPPI_ERR_INVALID, "NULL z / T_q");
     for (int i = 0; i < cnt * 12; ++i)
         if (!std::isfinite(T_q[i])) return fail(MPPI_ERR_INVALID, "non-finite T_q");
+    for (int i = 0; i < cnt * c.latent_dim; ++i)
+        if (!std::isfinite(z[i])) return fail(MPPI_ERR_INVALID, "non-finite z");
     cudaStream_t s = ctx->stream;
     if (c.latent_dim > 0)
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.z + (size_t)c0 * c.latent_dim, z, sizeof(float) * cnt * c.latent_dim,
@@ -427,12 +472,37 @@ mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const f
     if (!gate) launch_fold(ctx->p, ctx->b, c0, cnt, s);   // the analytic provider uses T_q only
     CUDA_TRY(ctx, cudaGetLastError());
     CUDA_TRY(ctx, cudaStreamSynchronize(s));   // host arrays may be reused on return
-    for (int i = 0; i < cnt; ++i) ctx->latent_set[c0 + i] = 1;
+    for (int i = 0; i < cnt; ++i) {
+        ctx->latent_set[c0 + i] = 1;
+        ctx->latent_t[c0 + i] = t_frame;
+        ctx->latent_steps[c0 + i] = 0;
+        ctx->latent_invalid[c0 + i] = 0;
+    }
+    return MPPI_OK;
+}
+
+mppi_status mppi_set_latent(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q) {
+    return set_latent_impl(ctx, ctrl, z, T_q, NAN, 1);
+}
+
+mppi_status mppi_set_latent_frame(mppi_ctx* ctx, int32_t ctrl, const float* z, const float* T_q, double t_frame,
+                                  int32_t valid) {
+    return set_latent_impl(ctx, ctrl, z, T_q, t_frame, valid);
+}
+
+mppi_status mppi_get_latent_status(mppi_ctx* ctx, double* out_t, int64_t* out_steps, int64_t* out_invalid) {
+    CHECK_CTX(ctx);
+    const int n = ctx->cfg.n_ctrl;
+    for (int i = 0; i < n; ++i) {
+        if (out_t) out_t[i] = ctx->latent_t[i];
+        if (out_steps) out_steps[i] = ctx->latent_steps[i];
+        if (out_invalid) out_invalid[i] = ctx->latent_invalid[i];
+    }
     return MPPI_OK;
 }
 
 mppi_status mppi_set_nominal(mppi_ctx* ctx, int32_t ctrl, const float* U) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     const mppi_config& c = ctx->cfg;
     if (ctrl < -1 || ctrl >= c.n_ctrl || !U) return fail(MPPI_ERR_INVALID, "bad ctrl / NULL");
     const int c0 = ctrl < 0 ? 0 : ctrl, cnt = ctrl < 0 ? c.n_ctrl : 1;
@@ -443,7 +513,7 @@ mppi_status mppi_set_nominal(mppi_ctx* ctx, int32_t ctrl, const float* U) {
 }
 
 mppi_status mppi_set_noise(mppi_ctx* ctx, const float* d_noise) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (ctx->cfg.noise_mode != MPPI_NOISE_EXTERNAL) return fail(MPPI_ERR_INVALID, "context is not in external-noise mode");
     if (!d_noise) return fail(MPPI_ERR_INVALID, "NULL noise");
     const mppi_config& c = ctx->cfg;
@@ -488,9 +558,9 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
         launch_softmin(p, ctx->b, true, s);
         mark(4);
         if (mode == 0) {
-            const size_t recn = (size_t)p.n_ctrl * (4 + 4 * p.T);
-            if (ncclAllGather(ctx->b.record, ctx->b.gathered, recn, ncclFloat, ctx->comm, s) != ncclSuccess)
-                return cudaErrorUnknown;
+            const size_t recn = (size_t)p.n_ctrl * (kRecHead + 4 * p.T);
+            ctx->nccl_err = ncclAllGather(ctx->b.record, ctx->b.gathered, recn, ncclFloat, ctx->comm, s);
+            if (ctx->nccl_err != ncclSuccess) return cudaErrorUnknown;   // reported as MPPI_ERR_NCCL
             launch_combine(p, ctx->b, ctx->b.gathered, ctx->cfg.world_size, s);
         }
     } else {
@@ -503,7 +573,7 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
 
 static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, uint64_t step, bool device_inputs,
                             int mode) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!ctx->weights && ctx->cfg.sdf_provider != MPPI_SDF_GATE) return fail(MPPI_ERR_NOT_READY, "weights not set");
     for (char v : ctx->latent_set)
         if (!v) return fail(MPPI_ERR_NOT_READY, "latent not set for every controller");
@@ -539,11 +609,14 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     if (!ctx->graph[mode]) {
         cudaGraph_t g;
         CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        ctx->nccl_err = ncclSuccess;
         cudaError_t e = enqueue_step(ctx, mode, s);
         cudaError_t e2 = cudaStreamEndCapture(s, &g);
         if (e != cudaSuccess) {
             if (e2 == cudaSuccess) cudaGraphDestroy(g);
             ctx->poisoned = true;
+            if (ctx->nccl_err != ncclSuccess)
+                return fail(MPPI_ERR_NCCL, std::string("step capture: ncclAllGather: ") + ncclGetErrorString(ctx->nccl_err));
             return fail(MPPI_ERR_CUDA, std::string("step capture: ") + cudaGetErrorString(e));
         }
         CUDA_TRY(ctx, e2);
@@ -552,6 +625,7 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
         CUDA_TRY(ctx, e3);
     }
     CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph[mode], s));
+    for (auto& a : ctx->latent_steps) ++a;
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_out, s));
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
     ctx->prof_valid = ctx->profiling > 0;
@@ -571,12 +645,12 @@ mppi_status mppi_step_local(mppi_ctx* ctx, const float* x0, const float* goal, u
     return run_step(ctx, x0, goal, step_index, false, 1);
 }
 
-int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? 4 + 4 * ctx->cfg.T : 0; }
+int32_t mppi_record_size(const mppi_ctx* ctx) { return ctx ? kRecHead + 4 * ctx->cfg.T : 0; }
 
 const float* mppi_get_record_device(const mppi_ctx* ctx) { return ctx ? ctx->b.record : nullptr; }
 
 mppi_status mppi_step_finish(mppi_ctx* ctx, const float* d_records, int32_t R) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!d_records || R < 1) return fail(MPPI_ERR_INVALID, "bad records");
     launch_combine(ctx->p, ctx->b, d_records, R, ctx->stream);
     CUDA_TRY(ctx, cudaGetLastError());
@@ -584,10 +658,18 @@ mppi_status mppi_step_finish(mppi_ctx* ctx, const float* d_records, int32_t R) {
 }
 
 mppi_status mppi_get_controls(mppi_ctx* ctx, float* U_out, float* u0_out) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!U_out) return fail(MPPI_ERR_INVALID, "NULL U_out");
     const mppi_config& c = ctx->cfg;
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->comm) {   // asynchronous communicator failures surface here
+        ncclResult_t ar = ncclSuccess;
+        NCCL_TRY(ctx, ncclCommGetAsyncError(ctx->comm, &ar));
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            ctx->poisoned = true;
+            return fail(MPPI_ERR_NCCL, std::string("communicator async error: ") + ncclGetErrorString(ar));
+        }
+    }
     CUDA_TRY(ctx, cudaMemcpy(U_out, ctx->b.U_out, sizeof(float) * c.n_ctrl * c.T * 4, cudaMemcpyDeviceToHost));
     if (u0_out)
         for (int i = 0; i < c.n_ctrl; ++i) std::memcpy(u0_out + 4 * i, U_out + (size_t)i * c.T * 4, 16);
@@ -599,7 +681,7 @@ mppi_status mppi_get_controls(mppi_ctx* ctx, float* U_out, float* u0_out) {
 }
 
 mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!out) return fail(MPPI_ERR_INVALID, "NULL out");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     CUDA_TRY(ctx, cudaMemcpy(out, ctx->b.diag, sizeof(float) * 4 * ctx->cfg.n_ctrl, cudaMemcpyDeviceToHost));
@@ -607,7 +689,7 @@ mppi_status mppi_get_diagnostics(mppi_ctx* ctx, float* out) {
 }
 
 mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t bytes) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     const Params& p = ctx->p;
     const size_t states = (size_t)p.n_ctrl * p.T * p.K;
     const void* src = nullptr;
@@ -623,7 +705,14 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
         case MPPI_DBG_NOISE: src = ctx->b.noise; need = 16 * states; break;
         case MPPI_DBG_TERMS: src = ctx->b.terms; need = 4 * states; break;
         case MPPI_DBG_PARTIAL: src = ctx->b.partial; need = 4 * (size_t)p.n_ctrl * p.K; break;
-        case MPPI_DBG_RECORD: src = ctx->b.record; need = 4 * (size_t)p.n_ctrl * (4 + 4 * p.T); break;
+        case MPPI_DBG_RECORD: src = ctx->b.record; need = 4 * (size_t)p.n_ctrl * (kRecHead + 4 * p.T); break;
+        case MPPI_DBG_WEIGHTS:
+            if (ctx->last_mode != 0) return fail(MPPI_ERR_NOT_READY, "MPPI_DBG_WEIGHTS needs a full mppi_step first");
+            launch_weights(p, ctx->b, ctx->stream);
+            CUDA_TRY(ctx, cudaGetLastError());
+            src = ctx->b.weights;
+            need = 4 * (size_t)p.n_ctrl * p.K;
+            break;
         default: return fail(MPPI_ERR_INVALID, "bad debug id");
     }
     if (!host_dst || bytes < need) return fail(MPPI_ERR_INVALID, "destination too small");
@@ -633,7 +722,7 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
 }
 
 mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int64_t n, float* d_out) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!ctx->weights) return fail(MPPI_ERR_NOT_READY, "weights not set");
     if (ctrl < 0 || ctrl >= ctx->cfg.n_ctrl || !ctx->latent_set[ctrl]) return fail(MPPI_ERR_NOT_READY, "latent not set");
     if (n < 0 || (n > 0 && (!d_rows || !d_out))) return fail(MPPI_ERR_INVALID, "bad rows/out");
@@ -651,7 +740,7 @@ mppi_status mppi_sdf_eval(mppi_ctx* ctx, int32_t ctrl, const float* d_rows, int6
 }
 
 mppi_status mppi_set_debug_outputs(mppi_ctx* ctx, int32_t on) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if ((on != 0) != (ctx->debug_outputs != 0)) {
         ctx->debug_outputs = on != 0;
         invalidate_graphs(ctx);
@@ -660,7 +749,7 @@ mppi_status mppi_set_debug_outputs(mppi_ctx* ctx, int32_t on) {
 }
 
 mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t level) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (level < 0 || level > 2) return fail(MPPI_ERR_INVALID, "profiling level must be 0, 1 or 2");
     if (level != ctx->profiling) {
         ctx->profiling = level;
@@ -670,7 +759,7 @@ mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t level) {
 }
 
 mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out) {
-    CHECK_CTX(ctx);
+    ENTER_CTX(ctx);
     if (!out || n_out < 1 || n_out > kNumStages) return fail(MPPI_ERR_INVALID, "bad out");
     if (!ctx->prof_valid) return fail(MPPI_ERR_NOT_READY, "no profiled step yet");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

@@ -6,6 +6,10 @@
 
 namespace mppi {
 
+// Softmin record: (m, S, S2, SJ, N, 0, 0, 0, V[T][4]) per controller -- min cost, sum of weights relative
+// to m, sum of squared weights, sum and count of the finite costs, weighted control deviations.
+constexpr int kRecHead = 8;
+
 // Per-step constants, passed by value to every kernel.
 struct Params {
     int n_ctrl, K, T;
@@ -14,6 +18,7 @@ struct Params {
     int act;              // MPPI_ACT_*
     int K_global;
     long long k_offset;
+    long long ctrl_offset;   // global index of this context's first controller (noise counters)
     float dt, inv_lambda, mass, gravity;
     float u_lo[4], u_hi[4], sigma[4];
     float w_goal, w_sdf, inv_sdf_scale, sdf_exp_max, w_u, w_guide, fd_h, inv_fd_h;
@@ -57,9 +62,10 @@ struct Buffers {
     float* partial;       // [n_ctrl*K] non-SDF cost sums
     float* J;             // [n_ctrl*K]
     unsigned* tickets;    // [n_ctrl] blocks of k_softmin done this step (reset by the last block)
-    float* blkrec;        // [n_ctrl][softmin blocks][4 + 4T] per-block records (m_b, S_b, S2_b, 0, V_b)
-    float* record;        // [n_ctrl][4 + 4T]  this rank's record (m_r, S_r, S2_r, 0, V_r)
-    float* gathered;      // [world][n_ctrl][4 + 4T]
+    float* blkrec;        // [n_ctrl][softmin blocks][kRecHead + 4T] per-block records
+    float* record;        // [n_ctrl][kRecHead + 4T]  this rank's record
+    float* gathered;      // [world][n_ctrl][kRecHead + 4T]
+    float* weights;       // [n_ctrl][K] normalised softmin weights (debug, on demand)
     float* diag;          // [n_ctrl][4]
     int* flags;           // [n_ctrl]
 };
@@ -73,6 +79,7 @@ void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaSt
 int softmin_blocks(int K);
 void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s);
 void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_count, cudaStream_t s);
+void launch_weights(const Params& p, const Buffers& b, cudaStream_t s);   // debug: normalised softmin weights
 // analytic Gate-SDF (Eq. 2) on the step's query rows -> SDF stage terms (replaces the MLP launch)
 void launch_sdf_gate(const Params& p, const Buffers& b, float* sdf_out, cudaStream_t s);
 

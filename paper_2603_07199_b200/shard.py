@@ -2,7 +2,7 @@
 
 configs[3]: the K samples of every controller are split evenly; rank r owns global samples
 [r K/R, (r+1) K/R) and keys its noise by global index, so the union of the shards is the unsharded
-iteration. The one exchange is the all-gather of the per-controller softmin record (m, S, S2, 0, V);
+iteration. The one exchange is the all-gather of the per-controller softmin record (m, S, S2, SJ, N, 0, 0, 0, V);
 every rank combines the records in rank order (k_combine / mppi_step_finish), so all ranks agree.
 configs[4]: the controllers are split evenly and nothing is exchanged (replicas of the data path).
 """

@@ -228,7 +228,7 @@ def test_all_nonfinite_leaves_controls_unchanged():
     assert ei.value.status == -5
     Ug, _ = ctrl.get_controls(allow_nonfinite=True)
     np.testing.assert_array_equal(Ug, inp["U"])
-    assert ctrl.diagnostics()[0, 3] == 1.0
+    assert np.isinf(ctrl.diagnostics()[0, 3])   # mean of the finite costs: none
 
 
 def test_not_ready_and_invalid():
