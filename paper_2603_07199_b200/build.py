@@ -32,6 +32,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False, trace: bool = False, extra: tuple = (), suffix: str = "") -> str:
     """trace=True builds the debug variant libmppi_b200_trace.so (-DMPPI_TC_TRACE kernel timeline)."""
     lib_out = LIB.replace(".so", ("_trace" if trace else "") + suffix + ".so")
+    if os.environ.get("MPPI_SKIP_BUILD") == "1" and not force:   # development runs against MPPI_LIB
+        return lib_out
     if not force and not trace and not suffix and not needs_build():
         return LIB
     inc, lib = nccl_dirs()

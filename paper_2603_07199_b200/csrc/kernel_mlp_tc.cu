@@ -764,8 +764,10 @@ bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands) {
     return pe_bands == 0 || (pe_bands == 4 && H == 128 && n_gemm >= 1 && n_gemm <= 3);
 }
 
+
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                           float* sdf_out, bool states_mode, cudaStream_t s) {
+    if (p.H == 128 && !p.mlp_legacy) return launch_mlp_h128(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
 #define MPPI_TC_CASE(HH, GG, AA) \
     if (p.H == HH && p.n_gemm == GG && p.act == AA) \
         return p.pe_bands == 0 ? tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \

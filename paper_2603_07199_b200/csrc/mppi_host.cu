@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -53,6 +54,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_B1F] = 4 * n * H;
     sz[B_HW32] = c->mlp_dtype == MPPI_MLP_FP32 ? 4 * G * H * H : 0;
     sz[B_HWBF] = c->mlp_dtype == MPPI_MLP_BF16 ? mlp_tc_weight_bytes((int)H, (int)G) : 0;
+    if (c->mlp_dtype == MPPI_MLP_BF16 && H == 128) sz[B_HWBF] = mlp_h128_image_bytes((int)G, c->pe_bands);
     sz[B_HB] = 4 * G * H;
     sz[B_WOUT] = 4 * H;
     sz[B_BOUT] = 16;
@@ -312,6 +314,10 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.q_gate = cfg->q_gate; p.q_vis = cfg->q_vis; p.q_sdf = cfg->q_sdf; p.d_safe = cfg->d_safe;
     p.sdf_provider = cfg->sdf_provider; p.gate_c = cfg->gate_c; p.gate_tana = cfg->gate_tana;
     p.pe_bands = cfg->pe_bands;
+    {
+        const char* lg = getenv("MPPI_H128_LEGACY");
+        p.mlp_legacy = lg && lg[0] == '1' ? 1 : 0;
+    }
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
     ctx->latent_set.assign(cfg->n_ctrl, 0);
     ctx->latent_t.assign(cfg->n_ctrl, NAN);
@@ -435,8 +441,10 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.b_out, bo.data(), sizeof(float) * 4, cudaMemcpyHostToDevice));
     if (G > 0) {
         if (bf) {
-            std::vector<uint8_t> img(mlp_tc_weight_bytes(H, G));
+            std::vector<uint8_t> img(H == 128 ? mlp_h128_image_bytes(G, c.pe_bands) : mlp_tc_weight_bytes(H, G));
             mlp_tc_pack_weights(H, G, c.activation, hw.data(), hb.data(), img.data());
+            // H = 128: the layer-1 B operand (exact bf16 splits of the position / PE columns) follows
+            if (H == 128) mlp_h128_pack_l1(c.pe_bands, c.activation, w1pe.data(), img.data() + mlp_tc_weight_bytes(H, G));
             CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_wbf, img.data(), img.size(), cudaMemcpyHostToDevice));
         } else {
             CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_w32, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice));
@@ -772,6 +780,9 @@ mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out) {
 
 int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
     if (!host_out || max_entries <= 0) return 0;
+    // H = 128 kernel (kernel_mlp_h128.cu) when MPPI_TRACE_H128=1, else the kernel_mlp_tc.cu timeline
+    const char* h = getenv("MPPI_TRACE_H128");
+    if (h && h[0] == '1') return mlp_h128_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
     return mlp_tc_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
 }
 

@@ -32,6 +32,7 @@ struct Params {
     int sdf_provider;
     float gate_c, gate_tana;
     int pe_bands;         // positional encoding bands (0 or 4)
+    int mlp_legacy;       // 1: H = 128 runs the round-1 kernel_mlp_tc form (A/B only, env MPPI_H128_LEGACY=1)
 };
 
 // Device buffers of one context (all inside the workspace).
@@ -96,5 +97,13 @@ void mlp_tc_pack_weights(int H, int n_gemm, int act, const float* W, const float
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                           float* sdf_out, bool states_mode, cudaStream_t s);
 bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands);
+
+// H = 128 tcgen05 SDF-MLP with shared-memory A operands and layer 1 on the tensor cores (kernel_mlp_h128.cu)
+bool mlp_h128_supported(int n_gemm, int pe_bands);
+int mlp_h128_trace_copy(unsigned long long* host, int max_entries);   // debug builds (MPPI_TC_TRACE) only
+size_t mlp_h128_image_bytes(int n_gemm, int pe_bands);   // hidden image (as mlp_tc_pack_weights) + layer-1 B
+void mlp_h128_pack_l1(int pe_bands, int act, const float* w1pos, uint8_t* out);
+cudaError_t launch_mlp_h128(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
+                            float* sdf_out, bool states_mode, cudaStream_t s);
 
 }  // namespace mppi

@@ -185,6 +185,15 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[16]) {
                  :
                  : "memory");
 }
+// empty asm tying 16 registers after a preceding tcgen05.wait::ld (volatile asms keep their order), so no use of
+// them is scheduled above the wait
+__device__ __forceinline__ void tmem_tie_regs(uint32_t (&r)[16]) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -206,6 +215,13 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 __device__ __forceinline__ uint64_t smem_desc_kmajor_noswz(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
            ((uint64_t)1 << 46);
+}
+// UMMA shared-memory descriptor: K-major, no swizzle, general strides: lbo = byte distance between the
+// 16-B core matrices adjacent in K, sbo = byte distance between adjacent 8-row groups (0: every 8-row group
+// reads the same core matrices, e.g. a constant operand).
+__device__ __forceinline__ uint64_t smem_desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
 }
 // Instruction descriptor kind::f16: D fp32, A/B bf16, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {

@@ -1,4 +1,5 @@
 """A/B timing of SDF-MLP kernel builds (not a test): python tests/ab_mlp.py LIB1 LIB2 ... [--cfg c2]
+A library argument may carry environment settings: path,VAR=VAL,... (e.g. lib.so,MPPI_H128_LEGACY=1).
 Runs each library in its own subprocess, interleaved A B A B (3 rounds), timing mppi_sdf_eval on the
 configs' full per-iteration row count with CUDA events and sampling the SM clock with nvidia-smi."""
 import json
@@ -37,7 +38,7 @@ def child(cfg_name):
     smi.terminate()
     clk = [float(x) for x in smi.communicate()[0].split()]
     H, G = cfg0.hidden, cfg0.n_hidden - 1
-    flop = 2 * (3 * H + G * H * H + H) * n
+    flop = 2 * ((3 + 6 * cfg0.pe_bands) * H + G * H * H + H) * n
     ms = float(np.median(ts))
     print(json.dumps({"ms": ms, "tflops": flop / ms / 1e9, "sm_mhz": float(np.median(clk)) if clk else None}))
 
@@ -53,7 +54,9 @@ def main():
     res = {l: [] for l in libs}
     for _ in range(3):
         for lib in libs:
-            env = dict(os.environ, MPPI_LIB=lib, AB_OUT=f"/tmp/ab_{os.path.basename(lib)}_{cfg}.npy")
+            path, *kv = lib.split(",")
+            env = dict(os.environ, MPPI_LIB=path, AB_OUT=f"/tmp/ab_{os.path.basename(lib)}_{cfg}.npy", MPPI_SKIP_BUILD="1",
+                       **dict(x.split("=", 1) for x in kv))
             out = subprocess.run([sys.executable, __file__, "--child", cfg], env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             res[lib].append(json.loads(line[-1]) if line else {"error": out.stderr[-300:]})

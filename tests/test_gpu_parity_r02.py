@@ -138,7 +138,7 @@ def test_full_row_sdf_parity_c2():
     err = np.abs(s.astype(np.float64) - ref)
     assert err.max() <= gh.ABS_SDF_BF16, err.max()
     # most rows agree to fp32 rounding; the rest carry single-ulp bf16 flips of tanh.approx activations
-    # (measured r02: 48.8% of rows within 1e-6, median 1.1e-6)
+    # (measured r02: 48.8% of the rows within 1e-6)
     assert np.median(err) <= 1e-5, np.median(err)
     assert np.mean(err <= 1e-6) >= 0.4, (np.mean(err <= 1e-6), np.percentile(err, [50, 90, 99, 99.9]))
     ctrl.close()
