@@ -39,16 +39,32 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, extra
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     tmp = lib_out + f".{os.getpid()}.tmp"
-    cmd = [nvcc, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", inc, "-I", os.path.join(ROOT, "include"),
-           *(["-DMPPI_TC_TRACE"] if trace else []), *extra, *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
+    flags = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include"),
+             *(["-DMPPI_TC_TRACE"] if trace else []), *extra]
+    # one nvcc per translation unit, in parallel (the two tensor-core kernels dominate), then one link
+    objs = [f"{tmp}.{os.path.basename(src)}.o" for src in sources()]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        return subprocess.run([nvcc, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(objs)) as ex:
+        results = list(ex.map(compile_one, zip(sources(), objs)))
+    r = None
+    for res in results:
+        if verbose or res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+    if all(res.returncode == 0 for res in results):
+        r = subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-L", lib,
+                            "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", tmp], capture_output=True, text=True)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    if r is None or r.returncode != 0:
+        if r is not None:
+            sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc build of libmppi_b200.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
     os.replace(tmp, lib_out)
     return lib_out
 

@@ -68,7 +68,10 @@ constexpr int kEpiWarp0 = 4;    // epilogue warp w reads TMEM lanes 32 (w % 4)
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);   // warp 0 MMA, warp 1 weight loader, 2-3 idle
 // setmaxnreg split of the CTA register pool (640 threads launched at 96 registers): warpgroup 0
 // (issuer, loader) 32, the four epilogue warpgroups 112: 128 x 32 + 512 x 112 = 640 x 96
-constexpr int kRegsCtl = 32, kRegsEpi = 112;
+#ifndef MPPI_REGS_CTL
+#define MPPI_REGS_CTL 56   // the issuer spills below ~56 (measured c3 -1.2% vs 32)
+#endif
+constexpr int kRegsCtl = MPPI_REGS_CTL, kRegsEpi = ((96 * 640 - 128 * MPPI_REGS_CTL) / 512) / 8 * 8;
 constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_ISSUER_WARP
 #define MPPI_ISSUER_WARP -1   // -1: per configuration (see the issuer); 0 / 1 force lane 0 / the warp form
@@ -81,6 +84,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #endif
 #ifndef MPPI_L1_SMEM
 #define MPPI_L1_SMEM 1
+#endif
+#ifndef MPPI_L1_MMA
+#define MPPI_L1_MMA 0   // H = 256: layer 1 as a K = 32 MMA on exact bf16 splits (see Cfg::L1M; A/B: +28% at configs[2])
 #endif
 constexpr int kTileRows = 128;
 
@@ -102,7 +108,11 @@ struct Cfg {
     static constexpr int TMEM_COLS = NSLOT * SLOT_COLS;      // = 512
     static constexpr int GW = kEpiWarps / NSLOT;             // epilogue warps per slot group (8)
     static constexpr int COLG = GW / 4;                      // column groups per TMEM lane quarter in a group
-    static constexpr int NROWBUF = 2 * NSLOT;                // query-row buffers (prefetch one slot-tile ahead)
+    // H = 256: layer 1 runs on the tensor cores like the hidden layers (two N-half units of K = 32: the exact
+    // three-part bf16 splits of p_c and W1p, six cross products per coordinate, as kernel_mlp_h128.cu), so its
+    // epilogue is a GEMM epilogue (D + b1', act, pack) instead of a CUDA-core 3-wide dot per neuron pair
+    static constexpr bool L1M = CG == 2 && PEB == 0 && MPPI_L1_MMA;
+    static constexpr int NROWBUF = L1M ? NSLOT : 2 * NSLOT;  // query-row buffers (L1M: |v| kept in registers)
     static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
@@ -126,8 +136,10 @@ struct Cfg {
     static constexpr int OFF_ONES = OFF_BIAS + BIAS_BYTES;           // [128 rows][16] bf16 ones tile
     static constexpr int OFF_WO = OFF_ONES + kTileRows * 32;         // [H] output weights
     static constexpr int OFF_W1XY = OFF_WO + 4 * H;                  // [H/2] (w0x, w1x, w0y, w1y) layer-1 positions, scaled
-    static constexpr int OFF_W1Z = OFF_W1XY + 8 * H;                 // [H/2] (w0z, w1z)
-    static constexpr int OFF_B1 = OFF_W1Z + 4 * H;                   // [NSLOT groups][H] folded bias b1', scaled
+    static constexpr int OFF_W1Z = OFF_W1XY + (L1M ? 0 : 8 * H);     // [H/2] (w0z, w1z)
+    static constexpr int BL1_TILE = RB * 32;                         // L1M: per (unit, K step) RB rows x 16 bf16
+    static constexpr int OFF_BL1 = OFF_W1Z + (L1M ? 0 : 4 * H);      // L1M: [NH][2 K steps] no-swizzle K-major
+    static constexpr int OFF_B1 = OFF_BL1 + (L1M ? NH * 2 * BL1_TILE : 0);   // [NSLOT groups][H] folded bias b1', scaled
     static constexpr int OFF_PE = OFF_B1 + NSLOT * 4 * H;            // PEB > 0: [H/2][NPE] float2 PE weights, scaled
     static constexpr int OFF_PART = OFF_PE + (PEB > 0 ? (H / 2) * NPE * 8 : 0);   // [NSLOT][COLG][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
@@ -175,6 +187,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
 
     // ---- setup
+    if constexpr (C::L1M) {
+        // layer-1 B operand of this CTA: rows = its RB neurons of each N-half unit, K = 32 columns pairing with
+        // the A columns (t = 0..5 per coordinate c, column 3 t + c): w_h, w_m, w_h, w_l, w_m, w_h (x kP)
+        for (int idx = threadIdx.x; idx < C::NH * C::RB; idx += kThreads) {
+            const int q = idx / C::RB, nn = idx % C::RB;
+            const float4 w = w1p[q * C::UN + (int)rank * C::RB + nn];
+            const float wc[3] = {w.x * kP, w.y * kP, w.z * kP};
+            uint16_t part[3][3];   // [h, m, l][c]
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const __nv_bfloat16 hb = __float2bfloat16_rn(wc[c]);
+                const float r1 = wc[c] - __bfloat162float(hb);
+                const __nv_bfloat16 mb = __float2bfloat16_rn(r1);
+                const __nv_bfloat16 lb = __float2bfloat16_rn(r1 - __bfloat162float(mb));
+                part[0][c] = __bfloat16_as_ushort(hb);
+                part[1][c] = __bfloat16_as_ushort(mb);
+                part[2][c] = __bfloat16_as_ushort(lb);
+            }
+            constexpr int kB[6] = {0, 1, 0, 2, 1, 0};   // B part of term t
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const uint16_t v = k >= 18 ? (uint16_t)0 : part[kB[k / 3]][k % 3];
+                const int st = k / 16, kk = k % 16;
+                *reinterpret_cast<uint16_t*>(smem + C::OFF_BL1 + (q * 2 + st) * C::BL1_TILE + (nn / 8) * 256 + (kk / 8) * 128 +
+                                             (nn % 8) * 16 + (kk % 8) * 2) = v;
+            }
+        }
+    } else
     for (int jp = threadIdx.x; jp < H / 2; jp += kThreads) {
         const float4 w0 = w1p[2 * jp], w1 = w1p[2 * jp + 1];
         s_w1xy[jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
@@ -258,20 +298,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             // before every unit but the first), so they follow from (tile n, l, h) and nothing spills from the
             // issuer's 32 registers (configs[2] -1.3%). H = 128: per-slot counters (the closed form measured
             // +15% at configs[1,4] with the lane-0 issuer).
-            constexpr uint32_t kAPerTile = C::A1S ? G - 1 : G;
+            constexpr uint32_t kAPerTile = C::A1S ? G - 1 : C::L1M ? G + 1 : G;
+            constexpr uint32_t kLay = C::L1M ? G + 1 : G;   // MMA layers per tile (L1M: layer 1 is one)
             uint32_t a_cnt[C::NSLOT] = {}, u_cnt[C::NSLOT] = {}, s_cnt[C::NSLOT] = {};
             mbar_wait<CG == 2>(bar(BAR_WREADY), 0);
             for (long long i0 = 0; i0 < n_my; i0 += C::NSLOT) {
                 const int ns = (int)min((long long)C::NSLOT, n_my - i0);
                 const uint32_t n = (uint32_t)(i0 / C::NSLOT);   // this slot-tile's index: barrier phases below
-                for (int l = 0; l < G; ++l)
+                for (int l = C::L1M ? -1 : 0; l < G; ++l)
                     for (int h = 0; h < C::NH; ++h)
                         for (int sl = 0; sl < ns; ++sl) {
                             TC_TRACE(0, 0, l, h, sl, i0);
                             const bool a_smem = C::A1S && l == 0;
+                            // layer index within the tile's A-ready sequence (L1M: the A1 operand is step 0)
+                            const uint32_t lp = (uint32_t)(C::L1M ? l + 1 : l);
                             if constexpr (CG == 2) {
-                                if (h == 0) mbar_wait_issuer(bar(C::SPLITK ? BAR_AK0 + sl : BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
-                                const uint32_t u = (n * G + (uint32_t)l) * C::NH + (uint32_t)h;
+                                if (h == 0) {
+                                    if (C::SPLITK && l >= 0) mbar_wait_issuer(bar(BAR_AK0 + sl), (n * G + (uint32_t)l) & 1u);
+                                    else mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + lp) & 1u);
+                                }
+                                const uint32_t u = (n * kLay + lp) * C::NH + (uint32_t)h;
                                 if (u > 0) mbar_wait_issuer(bar(BAR_DFREE + sl), (u - 1) & 1u);
                             } else {
                                 if (a_smem) mbar_wait_issuer(bar(BAR_SREADY + sl), (s_cnt[sl]++) & 1);
@@ -299,6 +345,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     }
                                 }
                             };
+                            if (C::L1M && l < 0) {   // layer 1: D = A1 (TMEM) x B1^T, K = 32 (bias b1' in the epilogue)
+                                if (!kWarpIssuer || elect_one()) {
+#pragma unroll
+                                    for (int st = 0; st < 2; ++st)
+                                        tc_mma_ts<CG>(d_t, a_t + (uint32_t)(st * 8),
+                                                      smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BL1 + (h * 2 + st) * C::BL1_TILE)),
+                                                      idesc, (uint32_t)st);
+                                    tc_commit<CG>(bar(BAR_MMA + sl));
+                                }
+                                if constexpr (kWarpIssuer) __syncwarp();
+                                TC_TRACE(0, 2, l, h, sl, i0);
+                                continue;
+                            }
                             // SPLITK: N-half 0 starts on K-half 0 of A; K-half 1 waits for the whole epilogue
                             const int j_mid = C::SPLITK && h == 0 ? H / 32 : H / 16;
                             if (!kWarpIssuer || elect_one()) {
@@ -310,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             if (C::SPLITK && h == 0) {
                                 if constexpr (kWarpIssuer) __syncwarp();
-                                mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + (uint32_t)l) & 1u);
+                                mbar_wait_issuer(bar(BAR_AREADY + sl), (n * kAPerTile + lp) & 1u);
                                 tc_fence_after();
                             }
                             if (!kWarpIssuer || elect_one()) {
@@ -491,14 +550,85 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
+        // L1M: the layer-1 MMA operand of tile i (exact bf16 splits of p_c, K = 32) -> the slot's A columns in
+        // TMEM; the tile's |v| and far-controller state are kept in registers for its epilogues
+        float vn_nx = 0.f;
+        const float* bfar_nx = nullptr;
+        bool any_far_nx = false;
+        auto prep = [&](long long i) {
+            const long long t1 = tile_of(i);
+            if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
+            mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
+            const float4 q = row_of(i);
+            vn_nx = q.w;
+            const long long row0 = tile_row0(t1);
+            const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            if (lo != staged) {   // uniform across the group; b1g of the previous tile is no longer read
+                named_bar_sync(1 + C::NSLOT + sl, gthreads);
+                for (int j = gtid; j < H; j += gthreads) b1g[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
+                staged = lo;
+            }
+            const long long row = row0 + row_in_tile;
+            const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            bfar_nx = bb != lo ? b1f + (size_t)bb * H : nullptr;
+            any_far_nx = __any_sync(0xFFFFFFFFu, bfar_nx != nullptr);
+            uint32_t hv[3], mv[3], lv[3];
+            const float pc[3] = {q.x, q.y, q.z};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const __nv_bfloat16 hb = __float2bfloat16_rn(pc[c]);
+                const float r1 = pc[c] - __bfloat162float(hb);
+                const __nv_bfloat16 mb = __float2bfloat16_rn(r1);
+                const __nv_bfloat16 lb = __float2bfloat16_rn(r1 - __bfloat162float(mb));
+                hv[c] = __bfloat16_as_ushort(hb);
+                mv[c] = __bfloat16_as_ushort(mb);
+                lv[c] = __bfloat16_as_ushort(lb);
+            }
+            // columns 3 t + c, t = 0..5: x_h, x_h, x_m, x_h, x_m, x_l (pairs with B: w_h, w_m, w_h, w_l, w_m, w_h);
+            // compile-time indices only (a runtime index sends the arrays to local memory)
+            uint32_t kv[16];
+#pragma unroll
+            for (int w2 = 0; w2 < 16; ++w2) {
+                uint32_t v2[2];
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const int k = 2 * w2 + e2, t = k / 3, c = k % 3;
+                    v2[e2] = k >= 18 ? 0u : (t == 2 || t == 4) ? mv[c] : t == 5 ? lv[c] : hv[c];
+                }
+                kv[w2] = v2[0] | (v2[1] << 16);
+            }
+            uint32_t a[8];
+#pragma unroll
+            for (int w2 = 0; w2 < 8; ++w2) a[w2] = cgi == 0 ? kv[w2] : kv[8 + w2];
+            tmem_st8(tmem + lane_addr + (uint32_t)(sl * C::SLOT_COLS + C::A_OFF + 8 * cgi), a);
+            named_bar_sync(1 + C::NSLOT + sl, gthreads);   // every warp has read the row buffer (and b1g is staged)
+            issue_rows(i + C::NSLOT);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_sched(BAR_AREADY + sl);
+            if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
+        };
+        float vn = 0.f;
+        const float* bfar_t = nullptr;
+        bool any_far_t = false;
         issue_rows(sl);
-        if constexpr (C::A1S) issue_rows(sl + C::NSLOT);
-        if (sl < n_my) layer1(sl);
+        if constexpr (C::L1M) {
+            if (sl < n_my) prep(sl);
+        } else {
+            if constexpr (C::A1S) issue_rows(sl + C::NSLOT);
+            if (sl < n_my) layer1(sl);
+        }
         for (long long i = sl; i < n_my; i += C::NSLOT) {
             uint32_t keep[C::NH > 1 ? C::QW / 2 : 1];   // unit-0 activations (bf16x2) until unit 1 is done
             float2 sdot2 = make_float2(0.f, 0.f);
+            if constexpr (C::L1M) {
+                vn = vn_nx;
+                bfar_t = bfar_nx;
+                any_far_t = any_far_nx;
+            }
 #pragma unroll 1
-            for (int l = 0; l < G; ++l) {
+            for (int l = C::L1M ? -1 : 0; l < G; ++l) {
                 const bool last = (l == G - 1);
 #pragma unroll
                 for (int h = 0; h < C::NH; ++h) {
@@ -506,6 +636,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(bar(BAR_MMA + sl), (mma_cnt++) & 1);
                     tc_fence_after();
                     if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
+                    // L1M: the tile's last MMA has read A -> next tile's layer-1 operand into the dead A columns
+                    if (C::L1M && last && h == C::NH - 1 && i + C::NSLOT < n_my) prep(i + C::NSLOT);
                     const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
                     const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
                     if (C::SPLITK && !last && h == C::NH - 1) {
@@ -543,11 +675,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int j0 = h * C::UN + cgi * C::QW + k * kCW;   // output neuron index
                         if (!last) {
                             uint32_t packed[kCW / 2];
+                            if (C::L1M && l < 0) {   // layer 1: D + kP b1' (per controller), fast path for one controller
+                                if (!any_far_t) {
+#pragma unroll
+                                    for (int i2 = 0; i2 < kCW; i2 += 4) {
+                                        const float4 bv = *reinterpret_cast<const float4*>(b1g + j0 + i2);
+                                        const float2 x0 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
+                                                                make_float2(1.f, 1.f), make_float2(bv.x, bv.y));
+                                        const float2 x1 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
+                                                                make_float2(1.f, 1.f), make_float2(bv.z, bv.w));
+                                        packed[i2 / 2] = act_pack<ACT>(x0.x, x0.y);
+                                        packed[i2 / 2 + 1] = act_pack<ACT>(x1.x, x1.y);
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int i2 = 0; i2 < kCW; i2 += 2) {
+                                        const float b0 = bfar_t ? __ldg(bfar_t + j0 + i2) * kP : b1g[j0 + i2];
+                                        const float b1 = bfar_t ? __ldg(bfar_t + j0 + i2 + 1) * kP : b1g[j0 + i2 + 1];
+                                        packed[i2 / 2] = act_pack<ACT>(__uint_as_float(acc[i2]) + b0, __uint_as_float(acc[i2 + 1]) + b1);
+                                    }
+                                }
+                            } else {
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
                                 // D = kP (W a + b): bias and pre-scale are already in the accumulator
                                 packed[i2 / 2] = act_pack<ACT>(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]));
                                 packed[i2 / 2 + 1] = act_pack<ACT>(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3]));
+                            }
                             }
                             if (h < C::NH - 1) {
 #pragma unroll
@@ -597,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.rps == 2) {
                         const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
                         const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                           p.w_guide * row_of(i).w * (s1 - sv) * p.inv_fd_h;
+                                           p.w_guide * (C::L1M ? vn : row_of(i).w) * (s1 - sv) * p.inv_fd_h;
                         if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
                     } else {
                         const float term = p.model == MPPI_MODEL_PAPER
@@ -609,7 +763,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
-            if constexpr (C::A1S) issue_rows(i + 2 * C::NSLOT);   // this tile's row buffer is free now
+            if constexpr (C::L1M) {
+            } else if constexpr (C::A1S) issue_rows(i + 2 * C::NSLOT);   // this tile's row buffer is free now
             else if (i + C::NSLOT < n_my) layer1(i + C::NSLOT);   // next tile of this slot; overlaps the others' MMAs
         }
     }
@@ -749,17 +904,6 @@ void mlp_tc_pack_weights(int H, int G, int act, const float* W, const float* hb,
             }
 }
 
-// positional encoding (4 bands) is instantiated for H = 128 only (its layer-1 weights need the smem H = 256
-// does not have)
-template <int HH, int GG, int AA>
-static cudaError_t pe_launch(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
-                             float* sdf_out, bool states_mode, cudaStream_t s) {
-    if constexpr (HH == 128) {
-        if (p.pe_bands == 4) return tc::launch_t<HH, GG, AA, 4>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
 bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands) {
     return pe_bands == 0 || (pe_bands == 4 && H == 128 && n_gemm >= 1 && n_gemm <= 3);
 }
@@ -771,7 +915,7 @@ cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows,
 #define MPPI_TC_CASE(HH, GG, AA) \
     if (p.H == HH && p.n_gemm == GG && p.act == AA) \
         return p.pe_bands == 0 ? tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \
-                               : pe_launch<HH, GG, AA>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+                               : cudaErrorInvalidValue;   /* PE: kernel_mlp_h128.cu (H = 128) only */
 #define MPPI_TC_ACTS(HH, GG) MPPI_TC_CASE(HH, GG, 0) MPPI_TC_CASE(HH, GG, 1) MPPI_TC_CASE(HH, GG, 2)
 #ifdef MPPI_TC_QUICK   // development builds: the configs[1..4] instantiations only
     MPPI_TC_CASE(128, 2, 1) MPPI_TC_CASE(256, 3, 2)
