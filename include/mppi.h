@@ -100,7 +100,7 @@ typedef struct {
     int32_t sdf_provider;                       /* MPPI_SDF_*                                       */
     float gate_c, gate_tana;                    /* MPPI_SDF_GATE: inner half-width c (m), tan(alpha) */
     int32_t pe_bands;                           /* positional encoding of the SDF input:
-                                                   0, or 4 (bf16 MLP with hidden 128): layer 1 reads
+                                                   0, or 4 (bf16 MLP, hidden 128 or 256): layer 1 reads
                                                    [p, sin(2^i pi p), cos(2^i pi p) (i < 4) | z], i.e.
                                                    in_dim[0] = 3 + 6 pe_bands + latent_dim (E1) */
     /* ABI 3 */

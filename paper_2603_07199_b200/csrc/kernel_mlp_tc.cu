@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "../../include/mppi.h"
 #include "mppi_internal.cuh"
@@ -140,8 +141,12 @@ struct Cfg {
     static constexpr int BL1_TILE = RB * 32;                         // L1M: per (unit, K step) RB rows x 16 bf16
     static constexpr int OFF_BL1 = OFF_W1Z + (L1M ? 0 : 4 * H);      // L1M: [NH][2 K steps] no-swizzle K-major
     static constexpr int OFF_B1 = OFF_BL1 + (L1M ? NH * 2 * BL1_TILE : 0);   // [NSLOT groups][H] folded bias b1', scaled
-    static constexpr int OFF_PE = OFF_B1 + NSLOT * 4 * H;            // PEB > 0: [H/2][NPE] float2 PE weights, scaled
-    static constexpr int OFF_PART = OFF_PE + (PEB > 0 ? (H / 2) * NPE * 8 : 0);   // [NSLOT][COLG][128] partial dots
+    // PEB > 0: [H/2][NPE] float2 PE weights (scaled) in shared memory at H = 128; at H = 256 the resident hidden
+    // weights leave no room, so layer 1 reads the same pair-major image from global memory (L1-cached,
+    // warp-uniform addresses)
+    static constexpr bool PE_SMEM = PEB > 0 && CG == 1;
+    static constexpr int OFF_PE = OFF_B1 + NSLOT * 4 * H;
+    static constexpr int OFF_PART = OFF_PE + (PE_SMEM ? (H / 2) * NPE * 8 : 0);   // [NSLOT][COLG][128] partial dots
     static constexpr int OFF_ROWS = OFF_PART + 4 * NSLOT * COLG * kTileRows;  // [NROWBUF][128] float4 query rows
     static constexpr int OFF_SA = A1S ? (OFF_ROWS + NROWBUF * 16 * kTileRows + 1023) / 1024 * 1024 : 0;
     static constexpr int SA_BYTES = kTileRows * H * 2;               // [K/64][128 rows][128 B] SW128 K-major
@@ -156,12 +161,24 @@ enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slo
        BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/, BAR_SREADY = 22 /*[slots]: smem layer-1 A tile*/,
        BAR_AK0 = 26 /*[slots]: K-half 0 of A written (SPLITK)*/ };
 
+// H = 256 with positional encoding: the pair-major layer-1 weights travel as a kernel parameter (27 KB of the
+// 32 KB parameter space, a per-launch copy in the constant bank): every epilogue thread reads the same weight at
+// the same time, which is the constant cache's broadcast case, and shared memory has no room left for them
+template <int NPAIR, int NPE>
+struct PEWeights {
+    float2 w[NPAIR * NPE];
+};
+struct NoPEWeights {};
+template <int H, int G, int PEB>
+using PEArg = typename std::conditional<(PEB > 0 && H == 256), PEWeights<H / 2, 3 + 6 * PEB>, NoPEWeights>::type;
+
 template <int H, int G, int ACT, int PEB>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_mlp_tc(Params p, const float4* __restrict__ rows, long long n_rows, int ctrl_fixed, int states_mode,
+    k_mlp_tc(const __grid_constant__ PEArg<H, G, PEB> pew, Params p, const float4* __restrict__ rows, long long n_rows,
+             int ctrl_fixed, int states_mode,
              const uint8_t* __restrict__ wimg, const float* __restrict__ hid_b, const float* __restrict__ w_out,
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
-             float* __restrict__ sdf_out, float* __restrict__ terms, const float* __restrict__ w1pe) {
+             float* __restrict__ sdf_out, float* __restrict__ terms, const float2* __restrict__ w1pe2) {
     using C = Cfg<H, G, PEB>;
     constexpr int CG = C::CG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -220,12 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_w1xy[jp] = make_float4(w0.x * kP, w1.x * kP, w0.y * kP, w1.y * kP);
         s_w1z[jp] = make_float2(w0.z * kP, w1.z * kP);
     }
-    if constexpr (PEB > 0) {   // [pair jp][feature f] = (W1[2jp][f], W1[2jp+1][f]) kP
+    if constexpr (C::PE_SMEM) {   // [pair jp][feature f] = (W1[2jp][f], W1[2jp+1][f]) kP
         float2* s_pe = reinterpret_cast<float2*>(smem + C::OFF_PE);
-        for (int i = threadIdx.x; i < (H / 2) * C::NPE; i += kThreads) {
-            const int jp = i / C::NPE, f = i % C::NPE;
-            s_pe[i] = make_float2(w1pe[(size_t)(2 * jp) * C::NPE + f] * kP, w1pe[(size_t)(2 * jp + 1) * C::NPE + f] * kP);
-        }
+        for (int i = threadIdx.x; i < (H / 2) * C::NPE; i += kThreads) s_pe[i] = w1pe2[i];
     }
     for (int r = threadIdx.x; r < kTileRows; r += kThreads) {   // ones tile: row r = [1, 1, 0 x 14] (bf16)
         uint32_t* o = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (r / 8) * 256 + (r % 8) * 16);
@@ -480,6 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sincospif(q.z * sc, &feat[3 + 6 * bnd + 2], &feat[3 + 6 * bnd + 5]);
                 }
                 const float2* s_pe = reinterpret_cast<const float2*>(smem + C::OFF_PE);
+                auto pe_w = [&](int idx) {
+                    if constexpr (C::PE_SMEM) return s_pe[idx];
+                    else return pew.w[idx];
+                };
 #pragma unroll
                 for (int c = 0; c < C::NH; ++c) {
 #pragma unroll
@@ -492,10 +510,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             float2 x = *reinterpret_cast<const float2*>(b1g + j0 + i2);
                             if (any_far && bfar) x = make_float2(__ldg(bfar + j0 + i2) * kP, __ldg(bfar + j0 + i2 + 1) * kP);
 #pragma unroll
-                            for (int f = 0; f < C::NPE; ++f) x = ffma2(s_pe[jp * C::NPE + f], make_float2(feat[f], feat[f]), x);
+                            for (int f = 0; f < C::NPE; ++f) x = ffma2(pe_w(jp * C::NPE + f), make_float2(feat[f], feat[f]), x);
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                         store_a1(j0, packed);
+                    }
+                    if (C::SPLITK && c == 0) {   // K-half 0 of the first GEMM's A is complete
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_sched(BAR_AK0 + sl);
                     }
                 }
             } else
@@ -825,10 +849,15 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     if (tiles == 0) return cudaSuccess;
     const long long groups = tiles < max_groups[dev] ? tiles : max_groups[dev];
     cfg.gridDim = dim3((unsigned)(groups * C::CG));
-    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB>, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
+    PEArg<H, G, PEB> pew{};
+    if constexpr (PEB > 0 && H == 256) {
+        if (!b.w1pe2_host) return cudaErrorInvalidValue;
+        std::memcpy(pew.w, b.w1pe2_host, sizeof(pew.w));
+    }
+    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB>, pew, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
                               (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,
                               (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms,
-                              (const float*)b.w1pe);
+                              (const float2*)b.w1pe2);
 }
 
 }  // namespace tc
@@ -905,7 +934,7 @@ void mlp_tc_pack_weights(int H, int G, int act, const float* W, const float* hb,
 }
 
 bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands) {
-    return pe_bands == 0 || (pe_bands == 4 && H == 128 && n_gemm >= 1 && n_gemm <= 3);
+    return pe_bands == 0 || (pe_bands == 4 && (H == 128 || H == 256) && n_gemm >= 1 && n_gemm <= 3);
 }
 
 
@@ -915,16 +944,21 @@ cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows,
 #define MPPI_TC_CASE(HH, GG, AA) \
     if (p.H == HH && p.n_gemm == GG && p.act == AA) \
         return p.pe_bands == 0 ? tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \
-                               : cudaErrorInvalidValue;   /* PE: kernel_mlp_h128.cu (H = 128) only */
+                               : tc::launch_t<HH, GG, AA, 4>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+#define MPPI_TC_CASE0(HH, GG, AA) \
+    if (p.H == HH && p.n_gemm == GG && p.act == AA && p.pe_bands == 0) \
+        return tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
 #define MPPI_TC_ACTS(HH, GG) MPPI_TC_CASE(HH, GG, 0) MPPI_TC_CASE(HH, GG, 1) MPPI_TC_CASE(HH, GG, 2)
-#ifdef MPPI_TC_QUICK   // development builds: the configs[1..4] instantiations only
-    MPPI_TC_CASE(128, 2, 1) MPPI_TC_CASE(256, 3, 2)
+    // H = 128 runs kernel_mlp_h128.cu; its round-1 form here stays for A/B (MPPI_H128_LEGACY=1, configs[1]/[4] MLP)
+    MPPI_TC_CASE0(128, 2, 1)
+#ifdef MPPI_TC_QUICK   // development builds: the configs[2..3] instantiations only
+    MPPI_TC_CASE(256, 3, 2)
 #else
-    MPPI_TC_ACTS(128, 1) MPPI_TC_ACTS(128, 2) MPPI_TC_ACTS(128, 3)
     MPPI_TC_ACTS(256, 1) MPPI_TC_ACTS(256, 2) MPPI_TC_ACTS(256, 3)
 #endif
 #undef MPPI_TC_ACTS
 #undef MPPI_TC_CASE
+#undef MPPI_TC_CASE0
     return cudaErrorInvalidValue;
 }
 

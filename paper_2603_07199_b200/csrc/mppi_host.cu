@@ -33,7 +33,7 @@ struct Layout {
 };
 
 enum BufId {
-    B_W1P, B_W1PE, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
+    B_W1P, B_W1PE, B_W1PE2, B_W1Z, B_B1, B_B1F, B_HW32, B_HWBF, B_HB, B_WOUT, B_BOUT, B_Z, B_TQ, B_X0, B_GOAL, B_STEP, B_UOUT,
     B_UNOM, B_NOISE, B_ROWS, B_SDF, B_TERMS, B_PART, B_J, B_TICK, B_BLKREC, B_REC, B_GATH, B_DIAG, B_FLAGS, B_WGT,
     B_COUNT
 };
@@ -49,6 +49,7 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     size_t sz[B_COUNT];
     sz[B_W1P] = 16 * H;
     sz[B_W1PE] = 4 * H * (size_t)(3 + 6 * c->pe_bands);
+    sz[B_W1PE2] = 4 * H * (size_t)(3 + 6 * c->pe_bands);
     sz[B_W1Z] = 4 * H * Ld;
     sz[B_B1] = 4 * H;
     sz[B_B1F] = 4 * n * H;
@@ -134,6 +135,7 @@ struct mppi_ctx {
     // latent cache status per controller: frame time, steps and invalid frames since
     std::vector<double> latent_t;
     std::vector<int64_t> latent_steps, latent_invalid;
+    std::vector<float> w1pe2_host;   // pair-major kPre-scaled layer-1 position/PE weights (kernel parameter)
 };
 
 // Every entry point that touches the device runs on the context's device and restores the caller's.
@@ -182,7 +184,7 @@ static mppi_status validate(const mppi_config* c) {
     if (c->sdf_provider != MPPI_SDF_MLP && c->sdf_provider != MPPI_SDF_GATE) return fail(MPPI_ERR_INVALID, "bad sdf_provider");
     if (c->pe_bands != 0 && c->pe_bands != 4) return fail(MPPI_ERR_UNSUPPORTED, "pe_bands must be 0 or 4");
     if (c->pe_bands && (c->mlp_dtype != MPPI_MLP_BF16 || !mlp_tc_pe_supported(c->hidden, c->n_hidden - 1, c->pe_bands)))
-        return fail(MPPI_ERR_UNSUPPORTED, "positional encoding: bf16 tcgen05 MLP with hidden 128 only");
+        return fail(MPPI_ERR_UNSUPPORTED, "positional encoding: bf16 tcgen05 MLP (hidden 128 or 256) only");
     if (c->sdf_provider == MPPI_SDF_GATE && (!std::isfinite(c->gate_c) || !(c->gate_tana >= 0.f) || !std::isfinite(c->gate_tana)))
         return fail(MPPI_ERR_INVALID, "gate_c finite, gate_tana >= 0");
     if (c->model == MPPI_MODEL_PAPER) {
@@ -265,6 +267,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     Buffers& b = ctx->b;
     b.w1p = (float4*)(base + L.off[B_W1P]);
     b.w1pe = (float*)(base + L.off[B_W1PE]);
+    b.w1pe2 = (float2*)(base + L.off[B_W1PE2]);
     b.w1z = (float*)(base + L.off[B_W1Z]);
     b.b1 = (float*)(base + L.off[B_B1]);
     b.b1f = (float*)(base + L.off[B_B1F]);
@@ -434,6 +437,19 @@ mppi_status mppi_set_sdf_weights(mppi_ctx* ctx, int32_t n_layers, const int32_t*
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1p, w1p.data(), sizeof(float4) * H, cudaMemcpyHostToDevice));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1pe, w1pe.data(), sizeof(float) * w1pe.size(), cudaMemcpyHostToDevice));
+    {   // neuron-pair-major, kPre-scaled copy of the position / PE columns (layer 1 of the H = 256 PE kernel)
+        const float kp = c.activation == MPPI_ACT_SILU ? 0.5f : 1.0f;
+        std::vector<float> w2((size_t)H * npe);
+        for (int jp = 0; jp < H / 2; ++jp)
+            for (int f = 0; f < npe; ++f) {
+                w2[((size_t)jp * npe + f) * 2] = w1pe[(size_t)(2 * jp) * npe + f] * kp;
+                w2[((size_t)jp * npe + f) * 2 + 1] = w1pe[(size_t)(2 * jp + 1) * npe + f] * kp;
+            }
+        CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1pe2, w2.data(), sizeof(float) * w2.size(), cudaMemcpyHostToDevice));
+        ctx->w1pe2_host = std::move(w2);
+        ctx->b.w1pe2_host = reinterpret_cast<const float2*>(ctx->w1pe2_host.data());
+        invalidate_graphs(ctx);   // the H = 256 PE kernel carries these weights in its launch parameters
+    }
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.w1z, w1z.data(), sizeof(float) * w1z.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(ctx, cudaMemcpy(ctx->b.b1, b1.data(), sizeof(float) * H, cudaMemcpyHostToDevice));
     if (G > 0) CUDA_TRY(ctx, cudaMemcpy(ctx->b.hid_b, hb.data(), sizeof(float) * hb.size(), cudaMemcpyHostToDevice));

@@ -40,6 +40,8 @@ struct Buffers {
     // MLP weights
     float4* w1p;          // [H] (W1[j][0..2], unused) layer-1 position columns
     float* w1pe;          // [H][3 + 6 pe_bands] layer-1 positional-encoding columns (pe_bands > 0)
+    float2* w1pe2;        // [H/2][3 + 6 pe_bands] the same, neuron-pair major, x kPre (H = 256 PE layer 1)
+    const float2* w1pe2_host;   // HOST copy of w1pe2 (launch-time kernel parameter of the H = 256 PE kernel)
     float* w1z;           // [H][L] layer-1 latent columns (for the fold)
     float* b1;            // [H]
     float* b1f;           // [n_ctrl][H] folded bias b1' = W1z z + b1

@@ -136,6 +136,9 @@ CONFIGS["c5gs"] = CONFIGS["c5s"].replace(name="c5gs", sdf_provider=1)
 # Positional encoding on the configs[1] MLP: 4 bands (27 position features)
 CONFIGS["c1pe"] = CONFIGS["c1"].replace(name="c1pe", pe_bands=4)
 CONFIGS["c1pes"] = CONFIGS["c1s"].replace(name="c1pes", pe_bands=4)
+# ... and on the configs[2]/[3] MLP (H = 256)
+CONFIGS["c2pe"] = CONFIGS["c2"].replace(name="c2pe", pe_bands=4)
+CONFIGS["c2pes"] = CONFIGS["c2s"].replace(name="c2pes", pe_bands=4)
 
 
 def get_config(name: str, **overrides) -> MPPIConfig:

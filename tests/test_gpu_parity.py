@@ -76,6 +76,7 @@ def test_tc_constructed_relu_net_is_exact(name):
     ("c1s", {"activation": 0}),                      # softplus on the tensor-core path
     ("c1pes", {}),                                   # positional encoding, 4 bands
     ("c1pes", {"n_hidden": 4, "activation": 2}),     # PE + SiLU, 3 GEMM layers
+    ("c2pes", {}),                                   # PE on the configs[2] MLP (H = 256, CTA pairs)
 ])
 def test_tc_random_weights_rows(name, over):
     cfg, Ws, bs, inp, ctrl = gh.setup(name, **over)
@@ -123,7 +124,7 @@ def _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref):
             assert gap <= tolJ[b][order[0]] + tolJ[b][order[1]], (d, gap)
 
 
-@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "c1pes"])
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "c1pes", "c2pes"])
 def test_bf16_step_parity(name):
     cfg, Ws, bs, inp, ctrl = gh.setup(name)
     ctrl.step(inp["x0"], inp["goal"], 0)
@@ -349,7 +350,7 @@ def test_sharded_ranks_match_unsharded_oracle(R):
     np.testing.assert_allclose(c1.get_controls()[0], outs[0], atol=1e-4)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c1pe"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c1pe", "c2pe"])
 def test_full_size_sampled_parity(name):
     """BASELINE configs[1..4] at full size with device noise (the bench's launch configuration): the
     oracle recomputes sampled rollouts one by one (global Philox counters) and their SDF rows and
