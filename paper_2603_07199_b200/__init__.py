@@ -200,3 +200,7 @@ class Controller:
 
     def kernels_per_step(self) -> int:
         return self.lib.mppi_kernels_per_step(self.ctx)
+
+    def fused_rollout(self) -> bool:
+        """True if the step runs the rollout inside the SDF-MLP kernel (query rows never reach HBM)."""
+        return bool(self.lib.mppi_fused_rollout(self.ctx))

@@ -23,7 +23,7 @@ EXPORTS = ["mppi_workspace_bytes", "mppi_create", "mppi_destroy", "mppi_get_nccl
            "mppi_set_sdf_weights", "mppi_set_latent", "mppi_set_latent_frame", "mppi_get_latent_status", "mppi_set_nominal", "mppi_set_noise", "mppi_step",
            "mppi_step_device", "mppi_step_local", "mppi_record_size", "mppi_get_record_device",
            "mppi_step_finish", "mppi_get_controls", "mppi_get_diagnostics", "mppi_debug_copy", "mppi_sdf_eval",
-           "mppi_set_profiling", "mppi_set_debug_outputs", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_debug_trace",
+           "mppi_set_profiling", "mppi_set_debug_outputs", "mppi_get_kernel_times", "mppi_kernels_per_step", "mppi_fused_rollout", "mppi_debug_trace",
            "mppi_last_error"]
 
 
@@ -95,6 +95,7 @@ def load(path: str | None = None):
         "mppi_set_debug_outputs": ([vp, i32], i32),
         "mppi_get_kernel_times": ([vp, vp, i32], i32),
         "mppi_kernels_per_step": ([vp], i32),
+        "mppi_fused_rollout": ([vp], i32),
         "mppi_debug_trace": ([vp, i32], i32),
         "mppi_last_error": ([], C.c_char_p),
     }

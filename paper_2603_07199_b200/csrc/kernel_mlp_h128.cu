@@ -37,6 +37,7 @@
 
 #include "../../include/mppi.h"
 #include "mppi_internal.cuh"
+#include "rollout_dev.cuh"
 #include "tc_ptx.cuh"
 
 namespace mppi {
@@ -55,6 +56,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_REGS_CTL
 #define H128_REGS_CTL 56
 #endif
+#ifndef H128_REGS_CTL_FUSE
+#define H128_REGS_CTL_FUSE 88
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -62,7 +66,7 @@ constexpr int kNB = H128_NB;    // 16-column loads per tcgen05.wait::ld
 
 constexpr int kSmemMax = 232448;
 
-template <int G, int PEB>
+template <int G, int PEB, bool FUSE = false>
 struct Cfg {
     static constexpr int NPE = 3 + 6 * PEB;                   // position features (raw p, PE bands)
     static constexpr int K1_USED = 18 + 18 * PEB;             // layer-1 operand columns (split products)
@@ -101,7 +105,8 @@ struct Cfg {
     static constexpr int THREADS = 32 * (4 + EPI_WARPS);
     // setmaxnreg split of the launch register pool (65536 / THREADS rounded to 8 per thread)
     static constexpr int REGS_LAUNCH = (65536 / THREADS) / 8 * 8;
-    static constexpr int REGS_CTL = REGS_LAUNCH >= 96 ? H128_REGS_CTL : 24;   // the issuer loop spills below ~48
+    // the issuer loop spills below ~48; FUSE: warps 2-3 of the same warpgroup run the rollout (~80 registers)
+    static constexpr int REGS_CTL = REGS_LAUNCH >= 96 ? (FUSE ? H128_REGS_CTL_FUSE : H128_REGS_CTL) : 24;
     static constexpr int REGS_EPI_RAW = (REGS_LAUNCH * THREADS - 128 * REGS_CTL) / (32 * EPI_WARPS) / 8 * 8;
     static constexpr int REGS_EPI = REGS_EPI_RAW > 232 ? 232 : REGS_EPI_RAW;
     static constexpr int TMEM_COLS = NSLOT * 128 <= 256 ? 256 : 512;
@@ -131,7 +136,7 @@ __device__ unsigned long long g_h128_trace[2][5][kTraceCap];
 #endif
 
 // barrier slots (8 B each)
-enum { BAR_ROWS = 0, BAR_SA1 = 4, BAR_AREADY = 8, BAR_DFREE = 12, BAR_MMA = 16, BAR_W = 20 };
+enum { BAR_ROWS = 0, BAR_SA1 = 4, BAR_AREADY = 8, BAR_DFREE = 12, BAR_MMA = 16, BAR_W = 20, BAR_RFREE = 21 };
 
 __device__ __forceinline__ uint32_t bf16_bits(float v) {
     return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
@@ -149,12 +154,17 @@ __device__ __forceinline__ void issuer_wait(uint32_t bar, uint32_t parity) {
 #endif
 }
 
-template <int G, int ACT, int PEB>
-__global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
+// FUSE (the fused rollout, configs[4]-sized problems): the rows are not read from HBM. Warps 2-3 of the control
+// warpgroup roll out 64 samples (a "block": one controller, samples k0..k0+63) over the whole horizon with the
+// same device code as k_rollout (rollout_dev.cuh) and write each step's 128 query rows straight into the next
+// slot's shared-memory row buffer; the CTA's tiles are (block, t) for its blocks in turn. The noise (for
+// k_softmin), the shifted nominal and the non-SDF partial costs go to HBM as k_rollout writes them.
+template <int G, int ACT, int PEB, bool FUSE>
+__global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
     k_mlp_h128(Params p, const float4* __restrict__ rows, long long n_rows, int ctrl_fixed, int states_mode,
                const uint8_t* __restrict__ wimg, const float* __restrict__ w_out, const float* __restrict__ b_out,
-               const float* __restrict__ b1f, float* __restrict__ sdf_out, float* __restrict__ terms) {
-    using C = Cfg<G, PEB>;
+               const float* __restrict__ b1f, float* __restrict__ sdf_out, float* __restrict__ terms, Buffers bufs) {
+    using C = Cfg<G, PEB, FUSE>;
     constexpr int NS = C::NSLOT;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -167,10 +177,23 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
     H_TRACE_DECL;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long n_tiles = (n_rows + kRows - 1) / kRows;
     const long long group = blockIdx.x, n_groups = gridDim.x;
-    const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
+    // FUSE: blocks of 64 samples (K % 64 == 0, guidance on: 128 rows per (block, t) tile)
+    const long long kb_per_ctrl = FUSE ? p.K / 64 : 1;
+    const long long n_units = FUSE ? (long long)p.n_ctrl * kb_per_ctrl : (n_rows + kRows - 1) / kRows;
+    const long long n_my_units = group < n_units ? (n_units - group + n_groups - 1) / n_groups : 0;
+    const long long n_my = FUSE ? n_my_units * p.T : n_my_units;   // local tiles
     const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
+    // first global row of local tile i (FUSE: tile = (block j, step t); rows of a state are adjacent)
+    auto row0_of = [&](long long i) -> long long {
+        if constexpr (FUSE) {
+            const long long j = i / p.T, t = i % p.T, blk = group + j * n_groups;
+            const long long bb = blk / kb_per_ctrl, k0 = (blk % kb_per_ctrl) * 64;
+            return ((bb * p.T + t) * p.K + k0) * 2;
+        } else {
+            return (group + i * n_groups) * kRows;
+        }
+    };
 
     // ---- setup: the ones operand of the bias MMA (one 8-row group, every group reads it: SBO = 0)
     if (threadIdx.x < 16) {
@@ -182,7 +205,8 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(bar(BAR_ROWS + s), 1);
+            mbar_init(bar(BAR_ROWS + s), FUSE ? 2 : 1);   // FUSE: the two rollout warps
+            mbar_init(bar(BAR_RFREE + s), 1);
             mbar_init(bar(BAR_SA1 + s), C::WPS);
             mbar_init(bar(BAR_AREADY + s), C::WPS);
             mbar_init(bar(BAR_DFREE + s), C::WPS);
@@ -209,6 +233,55 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
             for (int off = 0; off < C::IMG_BYTES; off += 32768) {
                 const int nb = C::IMG_BYTES - off < 32768 ? C::IMG_BYTES - off : 32768;
                 bulk_g2s(sbase + (uint32_t)off, wimg + off, (uint32_t)nb, bar(BAR_W));
+            }
+        } else if (FUSE && (warp == 2 || warp == 3) && n_my > 0) {
+            // ================= fused rollout producer: thread = one sample of the current block
+            const int tid = threadIdx.x - 64;
+            const unsigned long long step = *bufs.step;
+            const int sh = step > 0 ? 1 : 0;
+            const bool dev_noise = p.noise_device != 0;
+            const long long NK = (long long)p.n_ctrl * p.K;
+            const float inv_mass = 1.f / p.mass;
+            for (long long j = 0; j < n_my_units; ++j) {
+                const long long blk = group + j * n_groups;
+                const int bb = (int)(blk / kb_per_ctrl);
+                const int k = (int)((blk % kb_per_ctrl) * 64) + tid;
+                const bool first_block = blk % kb_per_ctrl == 0;
+                float x[10];
+#pragma unroll
+                for (int q = 0; q < 10; ++q) x[q] = __ldg(bufs.x0 + bb * 10 + q);
+                float R[9], tq[3], gc[3];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) R[q] = __ldg(bufs.Tq + bb * 12 + q);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) { tq[q] = __ldg(bufs.Tq + bb * 12 + 9 + q); gc[q] = __ldg(bufs.goal + bb * 3 + q); }
+                const long long col = (long long)bb * p.K + k;
+                const unsigned long long gidx = global_sample(p, bb, k);
+                const float4* Uo = reinterpret_cast<const float4*>(bufs.U_out) + (long long)bb * p.T;
+                float part = 0.f;
+                for (int t = 0; t < p.T; ++t) {
+                    const long long i = j * p.T + t;
+                    const int sl = (int)(i % NS);
+                    const uint32_t use = (uint32_t)(i / NS);
+                    const float4 U = Uo[min(t + sh, p.T - 1)];   // warm-start shift
+                    if (first_block && tid == 0) reinterpret_cast<float4*>(bufs.U_nom)[(long long)bb * p.T + t] = U;
+                    float4 n;
+                    if (dev_noise) {
+                        n = philox_normals(gidx, t, step, p.seed);
+                        bufs.noise[(long long)t * NK + col] = n;   // for k_softmin
+                    } else {
+                        n = bufs.noise[(long long)t * NK + col];
+                    }
+                    float4 row0, row1;
+                    ctbr_step(p, x, U, n, R, tq, gc, inv_mass, row0, row1, part);
+                    if (use > 0) mbar_wait(bar(BAR_RFREE + sl), (use - 1) & 1u);   // the slot has read its rows
+                    float4* dst = reinterpret_cast<float4*>(smem + C::OFF_ROWS + sl * 16 * kRows);
+                    dst[2 * tid] = row0;
+                    dst[2 * tid + 1] = row1;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_local(bar(BAR_ROWS + sl));
+                }
+                bufs.partial[col] = part;
             }
         } else if (warp == 0 && n_my > 0) {
             // ================= MMA issuer: per round of NS tiles, unit u = 0 (layer 1), 1..G (GEMMs), slots
@@ -280,11 +353,10 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
         float* b1s = reinterpret_cast<float*>(smem + C::OFF_B1S + sl * 4 * H);
         float* part = reinterpret_cast<float*>(smem + C::OFF_PART + sl * 4 * C::COLG * kRows);
         const bool leader = e == 0 && lane == 0;
-        auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto group_sync = [&]() { named_bar_sync(1 + sl, 32 * C::WPS); };
         auto issue_rows = [&](long long i) {   // query rows of local tile i -> this slot's row buffer (TMA engine)
-            if (!leader || i >= n_my) return;
-            const long long r0 = tile_of(i) * kRows;
+            if (FUSE || !leader || i >= n_my) return;   // FUSE: the rollout warps write the rows
+            const long long r0 = row0_of(i);
             const long long nv = min((long long)kRows, n_rows - r0);
             mbar_expect_tx(bar(BAR_ROWS + sl), (uint32_t)(16 * nv));
             bulk_g2s(sbase + (uint32_t)(C::OFF_ROWS + sl * 16 * kRows), rows + r0, (uint32_t)(16 * nv),
@@ -306,7 +378,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
             if (tracer) H_TRACE(1 + sl, 6, 0, i);
             const uint32_t rnd = (uint32_t)((i - sl) / NS);
             mbar_wait(bar(BAR_ROWS + sl), rnd & 1u);
-            const long long row = tile_of(i) * kRows + r;
+            const long long row = row0_of(i) + r;
             const float4 q = row < n_rows ? s_rows[r] : make_float4(0.f, 0.f, 0.f, 0.f);
             uint32_t col[C::K1];
 #pragma unroll
@@ -352,6 +424,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_local(bar(BAR_SA1 + sl));
             group_sync();                 // every warp of the group has read the row buffer
+            if (FUSE && leader) mbar_arrive_local(bar(BAR_RFREE + sl));
             issue_rows(i + NS);
             if (tracer) H_TRACE(1 + sl, 7, 0, i);
             return q.w;
@@ -379,7 +452,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
         if (sl < n_my) nv = build_a1(sl);
         const float bo = __ldg(b_out);
         for (long long i = sl; i < n_my; i += NS) {
-            const long long row0 = tile_of(i) * kRows;
+            const long long row0 = row0_of(i);
             // ---- layer-1 epilogue: x = D + b1' (per controller, x kPre), act, bf16 -> A of the first GEMM
             {
                 const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
@@ -537,33 +610,34 @@ __global__ void __launch_bounds__(Cfg<G, PEB>::THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
 }
 
-template <int G, int ACT, int PEB>
+template <int G, int ACT, int PEB, bool FUSE>
 cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s) {
-    using C = Cfg<G, PEB>;
+    using C = Cfg<G, PEB, FUSE>;
     constexpr int kMaxDev = 64;
     static int n_ctas[kMaxDev] = {};   // persistent grid per device (one CTA per SM); 0 = not set up
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
     if (n_ctas[dev] == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_mlp_h128<G, ACT, PEB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_mlp_h128<G, ACT, PEB, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
         if (e != cudaSuccess) return e;
         int n_sm = 0, per_sm = 0;
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_h128<G, ACT, PEB>, C::THREADS, C::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_h128<G, ACT, PEB, FUSE>, C::THREADS, C::SMEM);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
         n_ctas[dev] = n_sm;
         if (getenv("MPPI_VERBOSE"))
-            fprintf(stderr, "[mppi] k_mlp_h128<G=%d,ACT=%d,PEB=%d> dev %d: %d CTAs x %d threads, %d tiles in flight, smem %d B\n",
-                    G, ACT, PEB, dev, n_sm, C::THREADS, C::NSLOT, C::SMEM);
+            fprintf(stderr, "[mppi] k_mlp_h128<G=%d,ACT=%d,PEB=%d,FUSE=%d> dev %d: %d CTAs x %d threads, %d tiles in flight, smem %d B\n",
+                    G, ACT, PEB, (int)FUSE, dev, n_sm, C::THREADS, C::NSLOT, C::SMEM);
     }
-    const long long tiles = (n_rows + kRows - 1) / kRows;
-    if (tiles == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)(tiles < n_ctas[dev] ? tiles : n_ctas[dev]);
-    k_mlp_h128<G, ACT, PEB><<<grid, C::THREADS, C::SMEM, s>>>(p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
-                                                                (const uint8_t*)b.hid_wbf, b.w_out, b.b_out, b.b1f,
-                                                                sdf_out, b.terms);
+    const long long units = FUSE ? (long long)p.n_ctrl * (p.K / 64) : (n_rows + kRows - 1) / kRows;
+    if (units == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)(units < n_ctas[dev] ? units : n_ctas[dev]);
+    k_mlp_h128<G, ACT, PEB, FUSE><<<grid, C::THREADS, C::SMEM, s>>>(p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
+                                                                      (const uint8_t*)b.hid_wbf, b.w_out, b.b_out, b.b1f,
+                                                                      sdf_out, b.terms, b);
     return cudaGetLastError();
 }
 
@@ -640,11 +714,13 @@ void mlp_h128_pack_l1(int pe_bands, int act, const float* w1pos, uint8_t* out) {
 }
 
 cudaError_t launch_mlp_h128(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
-                            float* sdf_out, bool states_mode, cudaStream_t s) {
+                            float* sdf_out, bool states_mode, cudaStream_t s, bool fuse) {
 #define MPPI_H128_CASE(GG, AA)                                                                                  \
-    if (p.n_gemm == GG && p.act == AA)                                                                          \
-        return p.pe_bands == 4 ? h128::launch_t<GG, AA, 4>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \
-                               : h128::launch_t<GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+    if (p.n_gemm == GG && p.act == AA) {                                                                        \
+        if (fuse) return h128::launch_t<GG, AA, 0, true>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s); \
+        return p.pe_bands == 4 ? h128::launch_t<GG, AA, 4, false>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \
+                               : h128::launch_t<GG, AA, 0, false>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s); \
+    }
 #ifdef MPPI_TC_QUICK
     MPPI_H128_CASE(2, 1)
 #else

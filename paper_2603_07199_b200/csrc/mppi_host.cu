@@ -119,6 +119,8 @@ struct mppi_ctx {
     bool weights = false;
     std::vector<char> latent_set;
     bool use_tc = false;
+    bool fused = false;              // the step runs the rollout inside the H = 128 SDF-MLP kernel
+    bool last_fused = false;
     // pinned staging ring for x0 / goal / step
     float* h_stage[kStaging] = {};
     cudaEvent_t stage_ev[kStaging] = {};
@@ -317,11 +319,21 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     p.q_gate = cfg->q_gate; p.q_vis = cfg->q_vis; p.q_sdf = cfg->q_sdf; p.d_safe = cfg->d_safe;
     p.sdf_provider = cfg->sdf_provider; p.gate_c = cfg->gate_c; p.gate_tana = cfg->gate_tana;
     p.pe_bands = cfg->pe_bands;
+    p.noise_device = cfg->noise_mode == MPPI_NOISE_DEVICE ? 1 : 0;
     {
         const char* lg = getenv("MPPI_H128_LEGACY");
         p.mlp_legacy = lg && lg[0] == '1' ? 1 : 0;
     }
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
+    {   // fused rollout (kernel_mlp_h128.cu FUSE): the H = 128 CTBR path with guidance and K % 64 == 0. Opt-in
+        // (MPPI_FUSED=1): it removes the query-row round trip through HBM but measured slower at configs[4]
+        // (step 9.28 vs 8.87 ms: two producer warps per SM cannot integrate a step per tile as fast as the
+        // tensor pipe consumes the tiles)
+        const bool eligible = ctx->use_tc && cfg->hidden == 128 && cfg->pe_bands == 0 && cfg->model == MPPI_MODEL_BASELINE &&
+                              cfg->sdf_provider == MPPI_SDF_MLP && cfg->w_guide != 0.f && cfg->K % 64 == 0 && !p.mlp_legacy;
+        const char* fe = getenv("MPPI_FUSED");
+        ctx->fused = eligible && fe && fe[0] == '1';
+    }
     ctx->latent_set.assign(cfg->n_ctrl, 0);
     ctx->latent_t.assign(cfg->n_ctrl, NAN);
     ctx->latent_steps.assign(cfg->n_ctrl, 0);
@@ -567,10 +579,14 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     };
     mark(0);
     mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
-    launch_rollout(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
+    const bool fused = ctx->fused && !ctx->debug_outputs;   // debug outputs need the query rows in HBM
+    if (!fused) launch_rollout(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
     mark(2);
     cudaError_t e;
-    if (ctx->cfg.sdf_provider == MPPI_SDF_GATE) {
+    if (fused) {   // rollout + SDF-MLP in one kernel: the query rows never leave shared memory
+        const long long n_states = (long long)p.n_ctrl * p.T * p.K;
+        e = launch_mlp_h128(p, ctx->b, nullptr, n_states * p.rps, -1, nullptr, true, s, true);
+    } else if (ctx->cfg.sdf_provider == MPPI_SDF_GATE) {
         launch_sdf_gate(p, ctx->b, ctx->debug_outputs ? ctx->b.sdf_rows : nullptr, s);
         e = cudaGetLastError();
     } else {
@@ -654,6 +670,7 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
     ctx->prof_valid = ctx->profiling > 0;
     ctx->last_mode = mode;
+    ctx->last_fused = ctx->fused && !ctx->debug_outputs;
     return MPPI_OK;
 }
 
@@ -719,7 +736,11 @@ mppi_status mppi_debug_copy(mppi_ctx* ctx, int32_t what, void* host_dst, size_t 
     const void* src = nullptr;
     size_t need = 0;
     switch (what) {
-        case MPPI_DBG_QUERIES: src = ctx->b.rows; need = 16 * states * p.rps; break;
+        case MPPI_DBG_QUERIES:
+            if (ctx->last_fused) return fail(MPPI_ERR_NOT_READY, "query rows are not stored by the fused rollout (debug outputs off)");
+            src = ctx->b.rows;
+            need = 16 * states * p.rps;
+            break;
         case MPPI_DBG_SDF:
             if (!ctx->debug_outputs) return fail(MPPI_ERR_NOT_READY, "MPPI_DBG_SDF needs mppi_set_debug_outputs(ctx, 1)");
             src = ctx->b.sdf_rows;
@@ -804,8 +825,12 @@ int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
 
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx) {
     if (!ctx) return 0;
-    // rollout (+ noise + shift), mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL)
-    return 3 + (ctx->comm ? 1 : 0);
+    // rollout (+ noise + shift), mlp, softmin (cost + min + weights + update) (+ combine when sharded with NCCL);
+    // the fused rollout runs inside the mlp kernel
+    return (ctx->fused && !ctx->debug_outputs ? 2 : 3) + (ctx->comm ? 1 : 0);
+}
+
+int32_t mppi_fused_rollout(const mppi_ctx* ctx) { return ctx && ctx->fused && !ctx->debug_outputs ? 1 : 0;
 }
 
 }  // extern "C"

@@ -33,6 +33,7 @@ struct Params {
     float gate_c, gate_tana;
     int pe_bands;         // positional encoding bands (0 or 4)
     int mlp_legacy;       // 1: H = 128 runs the round-1 kernel_mlp_tc form (A/B only, env MPPI_H128_LEGACY=1)
+    int noise_device;     // MPPI_NOISE_DEVICE: the rollout generates the noise (and stores it for k_softmin)
 };
 
 // Device buffers of one context (all inside the workspace).
@@ -105,7 +106,8 @@ bool mlp_h128_supported(int n_gemm, int pe_bands);
 int mlp_h128_trace_copy(unsigned long long* host, int max_entries);   // debug builds (MPPI_TC_TRACE) only
 size_t mlp_h128_image_bytes(int n_gemm, int pe_bands);   // hidden image (as mlp_tc_pack_weights) + layer-1 B
 void mlp_h128_pack_l1(int pe_bands, int act, const float* w1pos, uint8_t* out);
+// fuse: the rollout runs inside the kernel (CTBR model, guidance on, K % 64 == 0, states_mode): rows unused
 cudaError_t launch_mlp_h128(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
-                            float* sdf_out, bool states_mode, cudaStream_t s);
+                            float* sdf_out, bool states_mode, cudaStream_t s, bool fuse = false);
 
 }  // namespace mppi
