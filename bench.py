@@ -396,8 +396,10 @@ def main():
                            "p99": float(np.percentile(r["step_ms"], 99))},
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": 1e3 * r["e2e_s"] / args.steps,
-                    "h2d_bytes_per_step": lcfg.n_ctrl * 13 * 4 + 8, "d2h_bytes_per_step": lcfg.n_ctrl * (cfg.T * 16 + 4),
-                    "note": "mppi_step (pinned staging H2D of x0, goal) + mppi_get_controls (D2H of U*), wall clock"},
+                    "h2d_bytes_per_step": (lcfg.n_ctrl * (cfg.state_dim + 3) * 4 + 7) // 8 * 8 + 8,
+                    "d2h_bytes_per_step": lcfg.n_ctrl * (cfg.T * 16 + 4),
+                    "note": "mppi_step (one pinned-staging H2D of [x0 | goal | step]) + mppi_get_controls (D2H of U* "
+                            "and the non-finite flags into pinned memory, one sync), wall clock"},
             "gpu_launches": args.steps * ctrl.kernels_per_step(),
             "clocks": r["clocks"]}
     ctrl.close()

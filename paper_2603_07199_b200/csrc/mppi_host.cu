@@ -40,6 +40,11 @@ enum BufId {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+int state_dim_of(const mppi_config* c) { return c->model == MPPI_MODEL_PAPER ? 17 : 10; }
+// bytes of x0 [n][sd] + goal [n][3], rounded up to 8 (the step index follows)
+size_t step_inputs_bytes(const mppi_config* c) { return ((size_t)4 * c->n_ctrl * (state_dim_of(c) + 3) + 7) / 8 * 8; }
+size_t step_block_bytes(const mppi_config* c) { return step_inputs_bytes(c) + 8; }
+
 bool compute_layout(const mppi_config* c, Layout* L) {
     const size_t n = (size_t)c->n_ctrl, K = (size_t)c->K, T = (size_t)c->T, H = (size_t)c->hidden;
     const size_t Ld = (size_t)c->latent_dim, G = (size_t)(c->n_hidden - 1);
@@ -61,9 +66,10 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_BOUT] = 16;
     sz[B_Z] = 4 * n * Ld;
     sz[B_TQ] = 4 * n * 12;
-    sz[B_X0] = 4 * n * (c->model == MPPI_MODEL_PAPER ? 17 : 10);
-    sz[B_GOAL] = 4 * n * 3;
-    sz[B_STEP] = 16;
+    // x0, goal and the step index are one contiguous block (one H2D copy per step): [x0 | goal | pad | step]
+    sz[B_X0] = step_block_bytes(c);
+    sz[B_GOAL] = 0;
+    sz[B_STEP] = 0;
     sz[B_UOUT] = 16 * n * T;
     sz[B_UNOM] = 16 * n * T;
     sz[B_NOISE] = 16 * T * n * K;
@@ -123,6 +129,7 @@ struct mppi_ctx {
     bool last_fused = false;
     // pinned staging ring for x0 / goal / step
     float* h_stage[kStaging] = {};
+    float* h_out = nullptr;          // pinned readback of U* [n_ctrl][T][4] and the flags [n_ctrl]
     cudaEvent_t stage_ev[kStaging] = {};
     int stage_i = 0;
     // graphs: [0] full step, [1] local (record) step
@@ -281,8 +288,8 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
     b.z = (float*)(base + L.off[B_Z]);
     b.Tq = (float*)(base + L.off[B_TQ]);
     b.x0 = (float*)(base + L.off[B_X0]);
-    b.goal = (float*)(base + L.off[B_GOAL]);
-    b.step = (unsigned long long*)(base + L.off[B_STEP]);
+    b.goal = b.x0 + (size_t)cfg->n_ctrl * state_dim_of(cfg);
+    b.step = (unsigned long long*)(base + L.off[B_X0] + step_inputs_bytes(cfg));
     b.U_out = (float*)(base + L.off[B_UOUT]);
     b.U_nom = (float*)(base + L.off[B_UNOM]);
     b.noise = (float4*)(base + L.off[B_NOISE]);
@@ -343,13 +350,16 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         mppi_destroy(ctx);
         return fail(s, m);
     };
-    const size_t stage_floats = (size_t)cfg->n_ctrl * (state_dim(cfg) + 3) + 4;
+    const size_t stage_floats = step_block_bytes(cfg) / 4 + 2;
     for (int i = 0; i < kStaging; ++i) {
         if (cudaHostAlloc((void**)&ctx->h_stage[i], stage_floats * sizeof(float), cudaHostAllocDefault) != cudaSuccess)
             return cleanup(MPPI_ERR_OOM, "cudaHostAlloc staging");
         if (cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming) != cudaSuccess)
             return cleanup(MPPI_ERR_CUDA, "cudaEventCreate");
     }
+    if (cudaHostAlloc((void**)&ctx->h_out, sizeof(float) * cfg->n_ctrl * cfg->T * 4 + sizeof(int) * cfg->n_ctrl,
+                      cudaHostAllocDefault) != cudaSuccess)
+        return cleanup(MPPI_ERR_OOM, "cudaHostAlloc readback");
     for (int i = 0; i <= kNumStages; ++i)
         if (cudaEventCreate(&ctx->prof_ev[i]) != cudaSuccess) return cleanup(MPPI_ERR_CUDA, "cudaEventCreate");
     if (cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking) != cudaSuccess ||
@@ -388,6 +398,7 @@ mppi_status mppi_destroy(mppi_ctx* ctx) {
         if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
         if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
     }
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
     for (auto& e : ctx->prof_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -630,7 +641,8 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
     if (device_inputs) {
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, x0, sizeof(float) * n * sd, cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, goal, sizeof(float) * n * 3, cudaMemcpyDeviceToDevice, s));
-        unsigned long long* hs = reinterpret_cast<unsigned long long*>(ctx->h_stage[ctx->stage_i] + (size_t)n * (sd + 3));
+        unsigned long long* hs =
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->h_stage[ctx->stage_i]) + step_inputs_bytes(&ctx->cfg));
         CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));
         *hs = step;
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, hs, 8, cudaMemcpyHostToDevice, s));
@@ -639,10 +651,9 @@ static mppi_status run_step(mppi_ctx* ctx, const float* x0, const float* goal, u
         CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[ctx->stage_i]));   // previous use of this slot done
         std::memcpy(h, x0, sizeof(float) * n * sd);
         std::memcpy(h + (size_t)n * sd, goal, sizeof(float) * n * 3);
-        *reinterpret_cast<unsigned long long*>(h + (size_t)n * (sd + 3)) = step;
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, h, sizeof(float) * n * sd, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.goal, h + (size_t)n * sd, sizeof(float) * n * 3, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.step, h + (size_t)n * (sd + 3), 8, cudaMemcpyHostToDevice, s));
+        std::memcpy(reinterpret_cast<char*>(h) + step_inputs_bytes(&ctx->cfg), &step, 8);
+        // one H2D copy of [x0 | goal | pad | step] (pinned staging ring; the device block has the same layout)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b.x0, h, step_block_bytes(&ctx->cfg), cudaMemcpyHostToDevice, s));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->stage_ev[ctx->stage_i], s));
     ctx->stage_i = (ctx->stage_i + 1) % kStaging;
@@ -711,13 +722,17 @@ mppi_status mppi_get_controls(mppi_ctx* ctx, float* U_out, float* u0_out) {
             return fail(MPPI_ERR_NCCL, std::string("communicator async error: ") + ncclGetErrorString(ar));
         }
     }
-    CUDA_TRY(ctx, cudaMemcpy(U_out, ctx->b.U_out, sizeof(float) * c.n_ctrl * c.T * 4, cudaMemcpyDeviceToHost));
+    // U* and the non-finite flags into pinned memory by two async copies on the stream, one synchronisation
+    const size_t u_bytes = sizeof(float) * c.n_ctrl * c.T * 4;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_out, ctx->b.U_out, u_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    int* h_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->h_out) + u_bytes);
+    CUDA_TRY(ctx, cudaMemcpyAsync(h_flags, ctx->b.flags, sizeof(int) * c.n_ctrl, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(U_out, ctx->h_out, u_bytes);
     if (u0_out)
         for (int i = 0; i < c.n_ctrl; ++i) std::memcpy(u0_out + 4 * i, U_out + (size_t)i * c.T * 4, 16);
-    std::vector<int> flags(c.n_ctrl);
-    CUDA_TRY(ctx, cudaMemcpy(flags.data(), ctx->b.flags, sizeof(int) * c.n_ctrl, cudaMemcpyDeviceToHost));
-    for (int f : flags)
-        if (f) return fail(MPPI_ERR_NONFINITE, "every J was non-finite for some controller; its U* is unchanged");
+    for (int i = 0; i < c.n_ctrl; ++i)
+        if (h_flags[i]) return fail(MPPI_ERR_NONFINITE, "every J was non-finite for some controller; its U* is unchanged");
     return MPPI_OK;
 }
 
