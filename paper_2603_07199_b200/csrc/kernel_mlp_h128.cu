@@ -59,6 +59,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_REGS_CTL_FUSE
 #define H128_REGS_CTL_FUSE 88
 #endif
+#ifndef H128_A1_HELPER
+#define H128_A1_HELPER 0   // 1: warps 2-3 build the layer-1 operands (measured +3% at configs[4]: off)
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -83,7 +86,10 @@ struct Cfg {
     static constexpr int QW = H / COLG;
     static constexpr int NCH = QW / kCW;                      // 16-column TMEM loads per thread per unit
     static constexpr int FIXED = IMG_BYTES + 256 + 4 * H + 8 * 32 + 16 + 1024;
-    static constexpr int PER_SLOT = A_BYTES + 16 * kRows + 4 * H + 4 * COLG * kRows;
+    // A1 helper (no PE, not fused): warps 2-3 build every tile's layer-1 operand as soon as the slot's last GEMM
+    // has read A, and keep |v| per row in a double-buffered slot array for the output epilogue
+    static constexpr bool HELPER = !FUSE && PEB == 0 && H128_A1_HELPER;
+    static constexpr int PER_SLOT = A_BYTES + 16 * kRows + 4 * H + 4 * COLG * kRows + 8 * kRows;
     static constexpr int fits(int n) { return FIXED + n * PER_SLOT <= kSmemMax && 4 + WPS * n <= 32; }
 #ifdef H128_NSLOT
     static constexpr int NSLOT = H128_NSLOT;
@@ -98,7 +104,8 @@ struct Cfg {
     static constexpr int OFF_WO = OFF_ROWS + NSLOT * 16 * kRows;
     static constexpr int OFF_B1S = OFF_WO + 4 * H;            // [NSLOT][H] staged b1' (x kPre)
     static constexpr int OFF_PART = OFF_B1S + NSLOT * 4 * H;  // [NSLOT][COLG][128] partial output dots
-    static constexpr int OFF_BAR = OFF_PART + NSLOT * 4 * COLG * kRows;
+    static constexpr int OFF_NV = OFF_PART + NSLOT * 4 * COLG * kRows;   // [NSLOT][2][128] |v| per row (HELPER)
+    static constexpr int OFF_BAR = OFF_NV + NSLOT * 8 * kRows;
     static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
     static constexpr int EPI_WARPS = WPS * NSLOT;
@@ -136,7 +143,8 @@ __device__ unsigned long long g_h128_trace[2][5][kTraceCap];
 #endif
 
 // barrier slots (8 B each)
-enum { BAR_ROWS = 0, BAR_SA1 = 4, BAR_AREADY = 8, BAR_DFREE = 12, BAR_MMA = 16, BAR_W = 20, BAR_RFREE = 21 };
+enum { BAR_ROWS = 0, BAR_SA1 = 4, BAR_AREADY = 8, BAR_DFREE = 12, BAR_MMA = 16, BAR_W = 20, BAR_RFREE = 21,
+       BAR_AFREE = 25 /*[slots]: the tile's last GEMM has read A (HELPER)*/ };
 
 __device__ __forceinline__ uint32_t bf16_bits(float v) {
     return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
@@ -207,7 +215,8 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
         for (int s = 0; s < NS; ++s) {
             mbar_init(bar(BAR_ROWS + s), FUSE ? 2 : 1);   // FUSE: the two rollout warps
             mbar_init(bar(BAR_RFREE + s), 1);
-            mbar_init(bar(BAR_SA1 + s), C::WPS);
+            mbar_init(bar(BAR_AFREE + s), 1);
+            mbar_init(bar(BAR_SA1 + s), C::HELPER ? 2 : C::WPS);
             mbar_init(bar(BAR_AREADY + s), C::WPS);
             mbar_init(bar(BAR_DFREE + s), C::WPS);
             mbar_init(bar(BAR_MMA + s), 1);
@@ -233,6 +242,61 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
             for (int off = 0; off < C::IMG_BYTES; off += 32768) {
                 const int nb = C::IMG_BYTES - off < 32768 ? C::IMG_BYTES - off : 32768;
                 bulk_g2s(sbase + (uint32_t)off, wimg + off, (uint32_t)nb, bar(BAR_W));
+            }
+        } else if (C::HELPER && (warp == 2 || warp == 3) && n_my > 0) {
+            // ================= layer-1 operand builder: tile i of slot i % NS as soon as the slot's last GEMM of
+            // tile i - NS has read A (BAR_AFREE, one commit per tile: it cannot run a phase ahead, because the
+            // slot's next MMA is this tile's layer 1, which waits for this builder), two rows per thread
+            const int tid = threadIdx.x - 64;
+            auto issue_rows_h = [&](long long i) {
+                if (i >= n_my) return;
+                const int s2 = (int)(i % NS);
+                const long long r0 = row0_of(i);
+                const long long nr = min((long long)kRows, n_rows - r0);
+                mbar_expect_tx(bar(BAR_ROWS + s2), (uint32_t)(16 * nr));
+                bulk_g2s(sbase + (uint32_t)(C::OFF_ROWS + s2 * 16 * kRows), rows + r0, (uint32_t)(16 * nr), bar(BAR_ROWS + s2));
+            };
+            if (tid == 0)
+                for (int s2 = 0; s2 < NS; ++s2) issue_rows_h(s2);
+            for (long long i = 0; i < n_my; ++i) {
+                const int sl = (int)(i % NS);
+                const uint32_t rnd = (uint32_t)(i / NS);
+                if (rnd > 0) mbar_wait(bar(BAR_AFREE + sl), (rnd - 1) & 1u);
+                mbar_wait(bar(BAR_ROWS + sl), rnd & 1u);
+                const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS + sl * 16 * kRows);
+                float* s_nv = reinterpret_cast<float*>(smem + C::OFF_NV + (sl * 2 + (int)(rnd & 1u)) * 4 * kRows);
+                const uint32_t aA = sbase + (uint32_t)(C::OFF_A + sl * C::A_BYTES);
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int r = tid + 64 * hf;
+                    const long long row = row0_of(i) + r;
+                    const float4 q = row < n_rows ? s_rows[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    s_nv[r] = q.w;
+                    uint32_t col[C::K1];
+#pragma unroll
+                    for (int k = 0; k < C::K1; ++k) col[k] = 0u;
+                    const float pv[3] = {q.x, q.y, q.z};
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const uint32_t h = bf16_bits(pv[c]);
+                        const float r1 = pv[c] - bf16_val(h);
+                        const uint32_t m = bf16_bits(r1);
+                        const uint32_t lo = bf16_bits(r1 - bf16_val(m));
+                        col[0 + c] = h; col[3 + c] = h; col[6 + c] = m; col[9 + c] = h; col[12 + c] = m; col[15 + c] = lo;
+                    }
+                    const uint32_t rb = aA + (uint32_t)((r / 8) * (C::K1C * 128) + (r % 8) * 16);
+#pragma unroll
+                    for (int kc = 0; kc < C::K1C; ++kc)
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (uint32_t)(kc * 128)),
+                                     "r"(col[8 * kc] | (col[8 * kc + 1] << 16)), "r"(col[8 * kc + 2] | (col[8 * kc + 3] << 16)),
+                                     "r"(col[8 * kc + 4] | (col[8 * kc + 5] << 16)), "r"(col[8 * kc + 6] | (col[8 * kc + 7] << 16))
+                                     : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA operand reads
+                named_bar_sync(7, 64);   // both builder warps have read the row buffer
+                if (tid == 0) issue_rows_h(i + NS);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_local(bar(BAR_SA1 + sl));
             }
         } else if (FUSE && (warp == 2 || warp == 3) && n_my > 0) {
             // ================= fused rollout producer: thread = one sample of the current block
@@ -331,6 +395,9 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                                 }
                             }
                             tc_commit<1>(bar(BAR_MMA + sl));
+                            // a second commit of the last GEMM for the layer-1 builder (its own barrier: waiting on
+                            // BAR_MMA's parity could alias a phase two commits back)
+                            if (C::HELPER && u == G) tc_commit<1>(bar(BAR_AFREE + sl));
                         }
                         __syncwarp();
                         if (lane == 0) H_TRACE(0, 2, u, i0 + sl);
@@ -448,8 +515,10 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
         uint32_t mma_cnt = 0;
         long long staged = -1;             // controller whose b1' is in b1s
         float nv = 0.f;                    // |v| of this thread's row of the current tile
-        issue_rows(sl);
-        if (sl < n_my) nv = build_a1(sl);
+        if constexpr (!C::HELPER) {
+            issue_rows(sl);
+            if (sl < n_my) nv = build_a1(sl);
+        }
         const float bo = __ldg(b_out);
         for (long long i = sl; i < n_my; i += NS) {
             const long long row0 = row0_of(i);
@@ -524,7 +593,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                 mbar_wait(bar(BAR_MMA + sl), (mma_cnt++) & 1u);
                 tc_fence_after();
                 if (tracer) H_TRACE(1 + sl, 4, l + 1, i);
-                if (last && i + NS < n_my) nv_next = build_a1(i + NS);   // the last GEMM has read A: next layer 1
+                if (!C::HELPER && last && i + NS < n_my) nv_next = build_a1(i + NS);   // the last GEMM has read A: next layer 1
                 uint32_t accb[2][kNB][kCW];
                 load_batch(0, accb[0]);
 #pragma unroll
@@ -571,6 +640,8 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                 }
                 if (tracer) H_TRACE(1 + sl, 5, l + 1, i);
             }
+            if constexpr (C::HELPER)   // |v| of this row, kept by the layer-1 builder
+                nv = reinterpret_cast<const float*>(smem + C::OFF_NV + (sl * 2 + (int)(((i - sl) / NS) & 1)) * 4 * kRows)[r];
             // ---- output of this tile: combine the column groups' partial dots, FD pair (adjacent lanes), term
             float sv = sdot.x + sdot.y;
             if constexpr (C::COLG > 1) {

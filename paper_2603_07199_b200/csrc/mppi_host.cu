@@ -589,8 +589,8 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
             cudaEventRecordWithFlags(ctx->prof_ev[i], s, cudaEventRecordExternal);
     };
     mark(0);
-    mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
     const bool fused = ctx->fused && !ctx->debug_outputs;   // debug outputs need the query rows in HBM
+    mark(1);   // noise generation and the warm-start shift are fused into the rollout kernel
     if (!fused) launch_rollout(p, ctx->b, ctx->cfg.noise_mode == MPPI_NOISE_DEVICE, s);
     mark(2);
     cudaError_t e;
