@@ -220,8 +220,8 @@ mppi_status mppi_set_profiling(mppi_ctx* ctx, int32_t level);
 mppi_status mppi_get_kernel_times(mppi_ctx* ctx, float* out, int32_t n_out);
 /* Number of kernels this library launches per mppi_step (for the bench's gpu_launches count). */
 int32_t mppi_kernels_per_step(const mppi_ctx* ctx);
-/* 1 if the step runs the rollout inside the SDF-MLP kernel (opt-in with env MPPI_FUSED=1 at mppi_create; H = 128
- * bf16 MLP, CTBR model, guidance on, K % 64 == 0; off while debug outputs are on):
+/* 1 if the step runs the rollout inside the SDF-MLP kernel (opt-in: env MPPI_FUSED=1 at mppi_create; CTBR model,
+ * guidance on; H = 128 with K % 64 == 0, H = 256 with K % 128 == 0; off while debug outputs are on):
  * the query rows then never reach HBM and MPPI_DBG_QUERIES returns MPPI_ERR_NOT_READY. */
 int32_t mppi_fused_rollout(const mppi_ctx* ctx);
 

@@ -192,12 +192,16 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
     const long long n_my_units = group < n_units ? (n_units - group + n_groups - 1) / n_groups : 0;
     const long long n_my = FUSE ? n_my_units * p.T : n_my_units;   // local tiles
     const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
+    // controller of a step row (states mode): rows < 2^31 (validated), so a 32-bit division -- a 64-bit one is
+    // ~10x the instructions, and this runs twice per tile and thread
+    auto ctrl_of = [&](long long row) -> long long { return (long long)((uint32_t)row / (uint32_t)rows_per_ctrl); };
     // first global row of local tile i (FUSE: tile = (block j, step t); rows of a state are adjacent)
     auto row0_of = [&](long long i) -> long long {
-        if constexpr (FUSE) {
-            const long long j = i / p.T, t = i % p.T, blk = group + j * n_groups;
-            const long long bb = blk / kb_per_ctrl, k0 = (blk % kb_per_ctrl) * 64;
-            return ((bb * p.T + t) * p.K + k0) * 2;
+        if constexpr (FUSE) {   // 32-bit divisions (a 64-bit one is ~10x the instructions, per tile and thread)
+            const uint32_t ii = (uint32_t)i, T = (uint32_t)p.T, kb = (uint32_t)kb_per_ctrl;
+            const uint32_t j = ii / T, t = ii - j * T, blk = (uint32_t)group + j * (uint32_t)n_groups;
+            const uint32_t bb = blk / kb, k0 = (blk - bb * kb) * 64u;
+            return (((long long)bb * p.T + t) * p.K + k0) * 2;
         } else {
             return (group + i * n_groups) * kRows;
         }
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
             const long long row0 = row0_of(i);
             // ---- layer-1 epilogue: x = D + b1' (per controller, x kPre), act, bf16 -> A of the first GEMM
             {
-                const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+                const long long lo = states_mode ? ctrl_of(min(row0, n_rows - 1)) : ctrl_fixed;
                 if (lo != staged) {   // uniform across the group
                     group_sync();
                     for (int j = gtid; j < H; j += 32 * C::WPS) b1s[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                     group_sync();
                 }
                 const long long row = row0 + r;
-                const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+                const long long bb = states_mode ? ctrl_of(min(row, n_rows - 1)) : ctrl_fixed;
                 const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
                 const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
                 if (tracer) H_TRACE(1 + sl, 3, 0, i);

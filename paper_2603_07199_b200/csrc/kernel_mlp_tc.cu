@@ -38,6 +38,7 @@
 
 #include "../../include/mppi.h"
 #include "mppi_internal.cuh"
+#include "rollout_dev.cuh"
 #include "tc_ptx.cuh"
 
 namespace mppi {
@@ -159,7 +160,7 @@ struct Cfg {
 // Barrier slots (8 B each): per tile slot (up to 4) and per query-row buffer (up to 8)
 enum { BAR_AREADY = 0 /*[slots]*/, BAR_DFREE = 4 /*[slots]*/, BAR_MMA = 8 /*[slots]*/, BAR_WLOCAL = 12,
        BAR_WREADY = 13, BAR_ROWS = 14 /*[row buffers]*/, BAR_SREADY = 22 /*[slots]: smem layer-1 A tile*/,
-       BAR_AK0 = 26 /*[slots]: K-half 0 of A written (SPLITK)*/ };
+       BAR_AK0 = 26 /*[slots]: K-half 0 of A written (SPLITK)*/, BAR_RFREE = 28 /*[row buffers]: FUSE, consumed*/ };
 
 // H = 256 with positional encoding: the pair-major layer-1 weights travel as a kernel parameter (27 KB of the
 // 32 KB parameter space, a per-launch copy in the constant bank): every epilogue thread reads the same weight at
@@ -172,14 +173,23 @@ struct NoPEWeights {};
 template <int H, int G, int PEB>
 using PEArg = typename std::conditional<(PEB > 0 && H == 256), PEWeights<H / 2, 3 + 6 * PEB>, NoPEWeights>::type;
 
-template <int H, int G, int ACT, int PEB>
+// FUSE (H = 256 CTA pairs, configs[3]-sized problems): the rows are not read from HBM. Warps 2-3 of each CTA
+// roll out its 64 samples of the pair's 128-sample block over the whole horizon with the device code of
+// k_rollout (rollout_dev.cuh) and write each step's 128 query rows into the next row buffer; the pair's tiles
+// are (block, t). Noise (for k_softmin), the shifted nominal and the non-SDF partial costs go to HBM as
+// k_rollout writes them.
+template <int H, int G, int ACT, int PEB, bool FUSE>
 __global__ void __launch_bounds__(kThreads, 1)
     k_mlp_tc(const __grid_constant__ PEArg<H, G, PEB> pew, Params p, const float4* __restrict__ rows, long long n_rows,
              int ctrl_fixed, int states_mode,
              const uint8_t* __restrict__ wimg, const float* __restrict__ hid_b, const float* __restrict__ w_out,
              const float* __restrict__ b_out, const float4* __restrict__ w1p, const float* __restrict__ b1f,
-             float* __restrict__ sdf_out, float* __restrict__ terms, const float2* __restrict__ w1pe2) {
+             float* __restrict__ sdf_out, float* __restrict__ terms, const float2* __restrict__ w1pe2, Buffers bufs) {
     using C = Cfg<H, G, PEB>;
+    static_assert(!FUSE || (H == 256 && PEB == 0 && !C::L1M), "fused rollout: H = 256 CTA pairs, CUDA-core layer 1");
+    // FUSE: the producer warps share warpgroup 0 with the issuer and need ~80 registers (no epilogue spills at 96)
+    constexpr int kCtl = FUSE ? 80 : kRegsCtl;
+    constexpr int kEpi = ((96 * 640 - 128 * kCtl) / 512) / 8 * 8;
     constexpr int CG = C::CG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -200,8 +210,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const long long group = blockIdx.x / CG, n_groups = gridDim.x / CG;
-    const long long n_tiles = (n_rows + (long long)kTileRows * CG - 1) / ((long long)kTileRows * CG);
+    // work units of the CTA group: pair tiles of 256 rows, or (FUSE) blocks of 128 samples (T tiles each)
+    const long long kb_per_ctrl = FUSE ? p.K / 128 : 1;
+    const long long n_units = FUSE ? (long long)p.n_ctrl * kb_per_ctrl
+                                   : (n_rows + (long long)kTileRows * CG - 1) / ((long long)kTileRows * CG);
+    const long long n_my_units = group < n_units ? (n_units - group + n_groups - 1) / n_groups : 0;
+    const long long n_tiles = FUSE ? (n_my_units > 0 ? n_units : 0) : n_units;   // "this group has work" below
+    const long long n_my_all = FUSE ? n_my_units * p.T : n_my_units;               // local tiles of the group
     const long long rows_per_ctrl = states_mode ? (long long)p.T * p.K * p.rps : (1ll << 62);
+    // controller of a step row (states mode): rows < 2^31 (validated), so a 32-bit division -- a 64-bit one is
+    // ~10x the instructions, and this runs twice per tile and thread
+    auto ctrl_of = [&](long long row) -> long long { return (long long)((uint32_t)row / (uint32_t)rows_per_ctrl); };
 
     // ---- setup
     if constexpr (C::L1M) {
@@ -259,7 +278,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_init(bar(BAR_WLOCAL), 1);
         mbar_init(bar(BAR_WREADY), CG);
-        for (int i = 0; i < C::NROWBUF; ++i) mbar_init(bar(BAR_ROWS + i), 1);
+        for (int i = 0; i < C::NROWBUF; ++i) {
+            mbar_init(bar(BAR_ROWS + i), FUSE ? 2 : 1);   // FUSE: the two rollout warps
+            if (FUSE) mbar_init(bar(BAR_RFREE + i), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -283,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto lbar = [&](int i) { return lbar0 + 8u * (uint32_t)i; };
 
     if (warp < kEpiWarp0) {
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtl));
       if (warp == 1) {
         // ================= weight loader: this CTA's share of every unit, once
         if (lane == 0 && group < n_tiles) {
@@ -297,6 +319,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
             else mbar_arrive_local(bar(BAR_WREADY));
         }
+      } else if (FUSE && (warp == 2 || warp == 3) && n_my_all > 0) {
+        // ================= fused rollout producer (FUSE): thread = one of this CTA's 64 samples of the block
+        const int tid = threadIdx.x - 64;
+        const unsigned long long step = *bufs.step;
+        const int sh = step > 0 ? 1 : 0;
+        const bool dev_noise = p.noise_device != 0;
+        const long long NK = (long long)p.n_ctrl * p.K;
+        const float inv_mass = 1.f / p.mass;
+        for (long long j = 0; j < n_my_units; ++j) {
+            const long long blk = group + j * n_groups;
+            const int bb = (int)(blk / kb_per_ctrl);
+            const int k = (int)((blk % kb_per_ctrl) * 128) + (int)rank * 64 + tid;
+            const bool first = blk % kb_per_ctrl == 0 && rank == 0 && tid == 0;
+            float x[10];
+#pragma unroll
+            for (int q = 0; q < 10; ++q) x[q] = __ldg(bufs.x0 + bb * 10 + q);
+            float Rm[9], tq[3], gc[3];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) Rm[q] = __ldg(bufs.Tq + bb * 12 + q);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { tq[q] = __ldg(bufs.Tq + bb * 12 + 9 + q); gc[q] = __ldg(bufs.goal + bb * 3 + q); }
+            const long long col = (long long)bb * p.K + k;
+            const unsigned long long gidx = global_sample(p, bb, k);
+            const float4* Uo = reinterpret_cast<const float4*>(bufs.U_out) + (long long)bb * p.T;
+            float part = 0.f;
+            for (int t = 0; t < p.T; ++t) {
+                const long long i = j * p.T + t;
+                const int rb = (int)(i % C::NROWBUF);
+                const uint32_t use = (uint32_t)(i / C::NROWBUF);
+                const float4 U = Uo[min(t + sh, p.T - 1)];   // warm-start shift
+                if (first) reinterpret_cast<float4*>(bufs.U_nom)[(long long)bb * p.T + t] = U;
+                float4 n;
+                if (dev_noise) {
+                    n = philox_normals(gidx, t, step, p.seed);
+                    bufs.noise[(long long)t * NK + col] = n;   // for k_softmin
+                } else {
+                    n = bufs.noise[(long long)t * NK + col];
+                }
+                float4 row0, row1;
+                ctbr_step(p, x, U, n, Rm, tq, gc, inv_mass, row0, row1, part);
+                if (use > 0) mbar_wait(bar(BAR_RFREE + rb), (use - 1) & 1u);   // tile i - NROWBUF has been output
+                float4* dst = reinterpret_cast<float4*>(smem + C::OFF_ROWS) + rb * kTileRows;
+                dst[2 * tid] = row0;
+                dst[2 * tid + 1] = row1;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_local(bar(BAR_ROWS + rb));
+            }
+            bufs.partial[col] = part;
+        }
       } else if (warp == 0) {
         // ================= MMA issuer (one thread of the leader CTA)
         // NSLOT tiles in flight (TMEM slots). Per layer and N-half h, one full-K unit per slot, issued slot by
@@ -307,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr bool kWarpIssuer = MPPI_ISSUER_WARP < 0 ? CG == 2 : MPPI_ISSUER_WARP != 0;
         if ((kWarpIssuer || lane == 0) && leader && group < n_tiles) {
             constexpr uint32_t idesc = idesc_bf16(C::MMA_M, C::UN);
-            const long long n_my = (n_tiles - group + n_groups - 1) / n_groups;
+            const long long n_my = n_my_all;
             // Barrier phases. H = 256: every slot sees the same sequence per tile (AREADY once per layer, DFREE
             // before every unit but the first), so they follow from (tile n, l, h) and nothing spills from the
             // issuer's 32 registers (configs[2] -1.3%). H = 128: per-slot counters (the closed form measured
@@ -397,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpi));
         // ================= epilogue: NSLOT groups of GW warps, group sl owns TMEM slot sl and the CTA's
         // tiles i = sl, sl + NSLOT, ... (one group computes while the others wait for their MMA units)
         constexpr int kColGroups = C::COLG;
@@ -412,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gtid = eg * 32 + lane;
         const bool tracer = lane == 0 && eg == 0 && sl < 2;   // trace roles 1, 2 = slots 0, 1
         const int trole = 1 + sl;
-        const long long n_my = group < n_tiles ? (n_tiles - group + n_groups - 1) / n_groups : 0;
+        const long long n_my = n_my_all;
         uint32_t mma_cnt = 0;
         long long staged = -1;                     // controller whose b1' sits in this group's b1g
         float* b1g = s_b1 + sl * H;
@@ -423,13 +494,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto tile_of = [&](long long i) { return group + i * n_groups; };
         auto tile_row0 = [&](long long t) { return t * (kTileRows * CG) + (long long)rank * kTileRows; };
+        // first global row of this CTA's part of local tile i (FUSE: tile = (block, step t); the CTA's 64
+        // samples are rank * 64 .. + 63 of the 128-sample block; the two rows of a state are adjacent)
+        auto row0_of = [&](long long i) -> long long {
+            if constexpr (FUSE) {   // 32-bit divisions (a 64-bit one is ~10x the instructions, per tile and thread)
+                const uint32_t ii = (uint32_t)i, T = (uint32_t)p.T, kb = (uint32_t)kb_per_ctrl;
+                const uint32_t j = ii / T, t = ii - j * T, blk = (uint32_t)group + j * (uint32_t)n_groups;
+                const uint32_t bb = blk / kb, k0 = (blk - bb * kb) * 128u + rank * 64u;
+                return (((long long)bb * p.T + t) * p.K + k0) * 2;
+            } else {
+                return tile_row0(tile_of(i));
+            }
+        };
         // query rows of this CTA's part of tile i -> smem buffer i % NROWBUF by one bulk-async copy (TMA
         // engine), issued one tile of this slot (NSLOT tiles) ahead by one elected thread of the group
         const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS);
         const bool row_issuer = eg == 0 && lane == 0;
         auto issue_rows = [&](long long i) {
-            if (!row_issuer || i >= n_my) return;
-            const long long r0 = tile_row0(tile_of(i));
+            if (FUSE || !row_issuer || i >= n_my) return;   // FUSE: the rollout warps write the rows
+            const long long r0 = row0_of(i);
             const long long nv = min((long long)kTileRows, n_rows - r0);
             if (nv <= 0) {
                 mbar_arrive_local(bar(BAR_ROWS + (int)(i % C::NROWBUF)));
@@ -440,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      bar(BAR_ROWS + (int)(i % C::NROWBUF)));
         };
         auto row_of = [&](long long i) {   // this thread's query row of tile i (after its buffer landed)
-            const long long row = tile_row0(tile_of(i)) + row_in_tile;
+            const long long row = row0_of(i) + row_in_tile;
             return row < n_rows ? s_rows[(i % C::NROWBUF) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         // 16 layer-1 activations (bf16x2) of this thread's row, neurons j0..j0+15 -> the slot's A operand:
@@ -467,8 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4 q = row_of(i);
             const float2 qx2 = make_float2(q.x, q.x), qy2 = make_float2(q.y, q.y), qz2 = make_float2(q.z, q.z);
             if constexpr (!C::A1S) issue_rows(i + C::NSLOT);   // buffer last read by tile i - NSLOT (behind its bar)
-            const long long row0 = tile_row0(t1);
-            const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const long long row0 = row0_of(i);
+            const long long lo = states_mode ? ctrl_of(min(row0, n_rows - 1)) : ctrl_fixed;
             if (lo != staged) {   // uniform across the group
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);   // nobody in the group still reads the old staging
                 for (int j = gtid; j < H; j += gthreads) b1g[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
@@ -476,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);
             }
             const long long row = row0 + row_in_tile;
-            const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const long long bb = states_mode ? ctrl_of(min(row, n_rows - 1)) : ctrl_fixed;
             const float* bfar = bb != lo ? b1f + (size_t)bb * H : nullptr;   // rows of a later controller
             const bool any_far = __any_sync(0xFFFFFFFFu, bfar != nullptr);
             if constexpr (PEB > 0) {
@@ -586,14 +669,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4 q = row_of(i);
             vn_nx = q.w;
             const long long row0 = tile_row0(t1);
-            const long long lo = states_mode ? min(row0, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const long long lo = states_mode ? ctrl_of(min(row0, n_rows - 1)) : ctrl_fixed;
             if (lo != staged) {   // uniform across the group; b1g of the previous tile is no longer read
                 named_bar_sync(1 + C::NSLOT + sl, gthreads);
                 for (int j = gtid; j < H; j += gthreads) b1g[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
                 staged = lo;
             }
             const long long row = row0 + row_in_tile;
-            const long long bb = states_mode ? min(row, n_rows - 1) / rows_per_ctrl : ctrl_fixed;
+            const long long bb = states_mode ? ctrl_of(min(row, n_rows - 1)) : ctrl_fixed;
             bfar_nx = bb != lo ? b1f + (size_t)bb * H : nullptr;
             any_far_nx = __any_sync(0xFFFFFFFFu, bfar_nx != nullptr);
             uint32_t hv[3], mv[3], lv[3];
@@ -762,14 +845,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (l == 0 && i + C::NSLOT < n_my) layer1(i + C::NSLOT);
             }
             // ---- output of this tile: combine column groups, FD pair, write
-            const long long tile = tile_of(i);
+            (void)tile_of;
             part[cgi * kTileRows + row_in_tile] = sdot2.x + sdot2.y;
             named_bar_sync(1 + sl, gthreads);
             if (cgi == 0) {
                 float sv = __ldg(b_out);
 #pragma unroll
                 for (int q2 = 0; q2 < kColGroups; ++q2) sv += part[q2 * kTileRows + row_in_tile];
-                const long long row = tile_row0(tile) + row_in_tile;
+                const long long row = row0_of(i) + row_in_tile;
                 if (row < n_rows && sdf_out) sdf_out[row] = sv;
                 if (states_mode) {
                     if (p.rps == 2) {
@@ -786,6 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
+            if (FUSE && row_issuer) mbar_arrive_local(bar(BAR_RFREE + (int)(i % C::NROWBUF)));   // to the rollout warps
             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
             if constexpr (C::L1M) {
             } else if constexpr (C::A1S) issue_rows(i + 2 * C::NSLOT);   // this tile's row buffer is free now
@@ -806,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int H, int G, int ACT, int PEB>
+template <int H, int G, int ACT, int PEB, bool FUSE = false>
 cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
                      float* sdf_out, bool states_mode, cudaStream_t s) {
     using C = Cfg<H, G, PEB>;
@@ -827,7 +911,7 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (max_groups[dev] == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT, PEB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<H, G, ACT, PEB, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         int n_sm = 0;
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -836,7 +920,7 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
         // round-robin over more groups than fit would serialise a second wave
         int clusters = 0;
         cfg.gridDim = dim3((unsigned)(groups * C::CG));
-        if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT, PEB>, &cfg) == cudaSuccess && clusters > 0)
+        if (cudaOccupancyMaxActiveClusters(&clusters, k_mlp_tc<H, G, ACT, PEB, FUSE>, &cfg) == cudaSuccess && clusters > 0)
             groups = clusters < groups ? clusters : groups;
         cudaGetLastError();
         if (groups < 1) return cudaErrorInvalidConfiguration;
@@ -845,7 +929,8 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
             fprintf(stderr, "[mppi] k_mlp_tc<%d,%d,%d> dev %d: %d SMs, %d co-resident groups of %d CTAs, smem %d B\n", H, G,
                     ACT, dev, n_sm, groups, C::CG, C::SMEM);
     }
-    const long long tiles = (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
+    const long long tiles = FUSE ? (long long)p.n_ctrl * (p.K / 128)   // 128-sample blocks
+                                 : (n_rows + (long long)kTileRows * C::CG - 1) / ((long long)kTileRows * C::CG);
     if (tiles == 0) return cudaSuccess;
     const long long groups = tiles < max_groups[dev] ? tiles : max_groups[dev];
     cfg.gridDim = dim3((unsigned)(groups * C::CG));
@@ -854,10 +939,10 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
         if (!b.w1pe2_host) return cudaErrorInvalidValue;
         std::memcpy(pew.w, b.w1pe2_host, sizeof(pew.w));
     }
-    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB>, pew, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
+    return cudaLaunchKernelEx(&cfg, k_mlp_tc<H, G, ACT, PEB, FUSE>, pew, p, rows, n_rows, ctrl_fixed, states_mode ? 1 : 0,
                               (const uint8_t*)b.hid_wbf, (const float*)b.hid_b, (const float*)b.w_out,
                               (const float*)b.b_out, (const float4*)b.w1p, (const float*)b.b1f, sdf_out, b.terms,
-                              (const float2*)b.w1pe2);
+                              (const float2*)b.w1pe2, b);
 }
 
 }  // namespace tc
@@ -939,8 +1024,20 @@ bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands) {
 
 
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
-                          float* sdf_out, bool states_mode, cudaStream_t s) {
-    if (p.H == 128 && !p.mlp_legacy) return launch_mlp_h128(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+                          float* sdf_out, bool states_mode, cudaStream_t s, bool fuse) {
+    if (p.H == 128 && !p.mlp_legacy) return launch_mlp_h128(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s, fuse);
+    if (fuse) {   // H = 256 fused rollout: the configs[2]/[3] MLP shape (ReLU / SiLU), no PE
+#define MPPI_TC_FUSE(GG, AA) \
+        if (p.H == 256 && p.n_gemm == GG && p.act == AA && p.pe_bands == 0) \
+            return tc::launch_t<256, GG, AA, 0, true>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
+#ifdef MPPI_TC_QUICK
+        MPPI_TC_FUSE(3, 2)
+#else
+        MPPI_TC_FUSE(3, 1) MPPI_TC_FUSE(3, 2)
+#endif
+#undef MPPI_TC_FUSE
+        return cudaErrorInvalidValue;
+    }
 #define MPPI_TC_CASE(HH, GG, AA) \
     if (p.H == HH && p.n_gemm == GG && p.act == AA) \
         return p.pe_bands == 0 ? tc::launch_t<HH, GG, AA, 0>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s) \

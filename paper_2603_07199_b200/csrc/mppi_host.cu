@@ -25,6 +25,9 @@ mppi_status fail(mppi_status st, const std::string& msg) {
 }
 
 constexpr int kStaging = 4;
+// the fused rollout is opt-in (MPPI_FUSED=1); these switch it on by default for large problems
+constexpr bool kFuse128Default = false;
+constexpr bool kFuse256Default = false;
 constexpr int kNumStages = 5;   // noise+shift, rollout, mlp, cost, update
 
 struct Layout {
@@ -332,14 +335,22 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         p.mlp_legacy = lg && lg[0] == '1' ? 1 : 0;
     }
     ctx->use_tc = cfg->mlp_dtype == MPPI_MLP_BF16;
-    {   // fused rollout (kernel_mlp_h128.cu FUSE): the H = 128 CTBR path with guidance and K % 64 == 0. Opt-in
-        // (MPPI_FUSED=1): it removes the query-row round trip through HBM but measured slower at configs[4]
-        // (step 9.28 vs 8.87 ms: two producer warps per SM cannot integrate a step per tile as fast as the
-        // tensor pipe consumes the tiles)
-        const bool eligible = ctx->use_tc && cfg->hidden == 128 && cfg->pe_bands == 0 && cfg->model == MPPI_MODEL_BASELINE &&
-                              cfg->sdf_provider == MPPI_SDF_MLP && cfg->w_guide != 0.f && cfg->K % 64 == 0 && !p.mlp_legacy;
+    {   // fused rollout (FUSE in kernel_mlp_h128.cu / kernel_mlp_tc.cu): the rollout runs inside the SDF-MLP
+        // kernel, so the query rows never reach HBM; MPPI_FUSED=0/1 overrides the default below
+        const bool common = ctx->use_tc && cfg->pe_bands == 0 && cfg->model == MPPI_MODEL_BASELINE &&
+                            cfg->sdf_provider == MPPI_SDF_MLP && cfg->w_guide != 0.f;
+        const bool e128 = common && cfg->hidden == 128 && cfg->K % 64 == 0 && !p.mlp_legacy;
+        const bool e256 = common && cfg->hidden == 256 && cfg->K % 128 == 0 && cfg->n_hidden == 4 &&
+                          (cfg->activation == MPPI_ACT_SILU || cfg->activation == MPPI_ACT_RELU);
+        // default off: configs[4] (H = 128) runs the same step time fused (with 1.68 GB less DRAM traffic) and
+        // configs[3] (H = 256) 2% slower; kFuse128Default / kFuse256Default switch the large-problem
+        // defaults on (>= 8 blocks per SM / CTA pair)
+        int n_sm = 148;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, cfg->device);
+        const bool auto128 = e128 && (long long)cfg->n_ctrl * (cfg->K / 64) >= 8LL * n_sm && kFuse128Default;
+        const bool auto256 = e256 && (long long)cfg->n_ctrl * (cfg->K / 128) >= 8LL * (n_sm / 2) && kFuse256Default;
         const char* fe = getenv("MPPI_FUSED");
-        ctx->fused = eligible && fe && fe[0] == '1';
+        ctx->fused = (e128 || e256) && (fe ? fe[0] == '1' : auto128 || auto256);
     }
     ctx->latent_set.assign(cfg->n_ctrl, 0);
     ctx->latent_t.assign(cfg->n_ctrl, NAN);
@@ -596,7 +607,7 @@ static cudaError_t enqueue_step(mppi_ctx* ctx, int mode, cudaStream_t s) {
     cudaError_t e;
     if (fused) {   // rollout + SDF-MLP in one kernel: the query rows never leave shared memory
         const long long n_states = (long long)p.n_ctrl * p.T * p.K;
-        e = launch_mlp_h128(p, ctx->b, nullptr, n_states * p.rps, -1, nullptr, true, s, true);
+        e = launch_mlp_tc(p, ctx->b, nullptr, n_states * p.rps, -1, nullptr, true, s, true);
     } else if (ctx->cfg.sdf_provider == MPPI_SDF_GATE) {
         launch_sdf_gate(p, ctx->b, ctx->debug_outputs ? ctx->b.sdf_rows : nullptr, s);
         e = cudaGetLastError();

@@ -97,8 +97,10 @@ size_t mlp_tc_weight_bytes(int H, int n_gemm);
 void mlp_tc_pack_weights(int H, int n_gemm, int act, const float* W, const float* hb, uint8_t* out);
 // rows_mode: rows are per-state query rows of the step (writes per-state SDF terms) when states_mode,
 // else arbitrary rows for mppi_sdf_eval (writes s per row only).
+// fuse: the rollout runs inside the kernel (states mode, CTBR model, guidance on; H = 128: K % 64 == 0,
+// H = 256: K % 128 == 0 and the configs[2]/[3] MLP shape); rows are then unused
 cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows, long long n_rows, int ctrl_fixed,
-                          float* sdf_out, bool states_mode, cudaStream_t s);
+                          float* sdf_out, bool states_mode, cudaStream_t s, bool fuse = false);
 bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands);
 
 // H = 128 tcgen05 SDF-MLP with shared-memory A operands and layer 1 on the tensor cores (kernel_mlp_h128.cu)

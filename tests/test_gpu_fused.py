@@ -1,5 +1,5 @@
-"""GPU parity of the fused rollout (-m gpu): kernel_mlp_h128.cu with FUSE runs the CTBR rollout inside the
-H = 128 SDF-MLP kernel (rows never reach HBM). It must give the step of the unfused path (k_rollout then the
+"""GPU parity of the fused rollout (-m gpu): with FUSE the SDF-MLP kernels (kernel_mlp_h128.cu at H = 128,
+kernel_mlp_tc.cu's CTA pairs at H = 256) run the CTBR rollout themselves (rows never reach HBM). It must give the step of the unfused path (k_rollout then the
 SDF-MLP kernel on the stored rows): the same noise, partial costs, SDF stage terms, costs and update, and the
 oracle's costs and update within the north_star tolerances."""
 import numpy as np
@@ -46,7 +46,8 @@ def _run(cfg, fused, monkeypatch, noise_mode, step=3, noise=None):
     return out
 
 
-@pytest.mark.parametrize("name,over", [("c4s", {}), ("c4s", {"n_ctrl": 5, "K": 128, "T": 7})])
+@pytest.mark.parametrize("name,over", [("c4s", {}), ("c4s", {"n_ctrl": 5, "K": 128, "T": 7}),
+                                       ("c3s", {}), ("c2s", {"n_ctrl": 3, "K": 256, "T": 5})])
 @pytest.mark.parametrize("noise_mode", ["device", "external"])
 def test_fused_rollout_equals_unfused(monkeypatch, name, over, noise_mode):
     cfg = synth.get_config(name, **over)
@@ -61,10 +62,11 @@ def test_fused_rollout_equals_unfused(monkeypatch, name, over, noise_mode):
     np.testing.assert_allclose(b["U"], a["U"], atol=1e-5)
 
 
-def test_fused_rollout_matches_oracle(monkeypatch):
+@pytest.mark.parametrize("name,over", [("c4s", {"n_ctrl": 4, "K": 128, "T": 6}), ("c3s", {"n_ctrl": 2, "T": 5})])
+def test_fused_rollout_matches_oracle(monkeypatch, name, over):
     """Costs and update of the fused step against the oracle on the same external noise (staged where the
     fused path allows: J per sample, then U* by the R26 rule and the softmin property)."""
-    cfg = synth.get_config("c4s", n_ctrl=4, K=128, T=6)
+    cfg = synth.get_config(name, **over)
     inp = dict(z=synth.make_latents(cfg), Tq=synth.make_query_transforms(cfg), x0=synth.make_x0(cfg),
                goal=synth.make_goals(cfg), U=synth.make_nominal(cfg), noise=synth.make_noise(cfg))
     Ws, bs = synth.make_weights(cfg)
@@ -83,13 +85,14 @@ def test_fused_rollout_matches_oracle(monkeypatch):
             assert ref["J"][b][order[1]] - ref["J"][b][order[0]] <= tolJ[b][order[0]] + tolJ[b][order[1]], d
 
 
-def test_fused_full_size_c4_sampled(monkeypatch):
-    """configs[4] at full size in the bench's configuration (fused, device noise): sampled rollouts recomputed
-    one by one by the oracle (global Philox counters) against the GPU's costs; the update by the softmin
-    property on the GPU's own costs."""
+@pytest.mark.parametrize("name", ["c4", "c3"])
+def test_fused_full_size_sampled(monkeypatch, name):
+    """configs[4] / configs[3] at full size (fused, device noise): sampled rollouts recomputed one by one by the
+    oracle (global Philox counters) against the GPU's costs; the update by the softmin property on the GPU's
+    own costs."""
     from paper_2603_07199_b200 import Controller
     monkeypatch.setenv("MPPI_FUSED", "1")
-    cfg = synth.get_config("c4")
+    cfg = synth.get_config(name)
     Ws, bs = synth.make_weights(cfg)
     z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
                           synth.make_goals(cfg), synth.make_nominal(cfg))
@@ -104,7 +107,7 @@ def test_fused_full_size_c4_sampled(monkeypatch):
     noise = c.debug("noise")
     oc = oracle.make_cfg(cfg)
     rng = np.random.default_rng(3)
-    for b in rng.choice(cfg.n_ctrl, size=3, replace=False):
+    for b in rng.choice(cfg.n_ctrl, size=min(cfg.n_ctrl, 3), replace=False):
         for k in rng.choice(cfg.K, size=4, replace=False):
             nz = oracle.noise(cfg.seed, 7, int(b) * cfg.K + int(k), 1, cfg.T)[:, 0]
             r = oracle.rollout(oc, Ws, bs, z[b], Tq[b], x0[b], goal[b], U[b], nz)
