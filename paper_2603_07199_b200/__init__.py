@@ -33,7 +33,7 @@ class Controller:
 
     def __init__(self, cfg, *, device: int = 0, stream=None, noise_mode: str = "device", world_size: int = 1,
                  rank: int = 0, K_global: int | None = None, k_offset: int = 0, nccl_id: bytes | None = None,
-                 seed: int | None = None, debug_outputs: bool = False, ctrl_offset: int = 0):
+                 seed: int | None = None, debug_outputs: bool = False, ctrl_offset: int = 0, guard_bytes: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2603_07199_b200.Controller needs a CUDA device (no CPU fallback)")
@@ -50,10 +50,16 @@ class Controller:
         nbytes = self.lib.mppi_workspace_bytes(C.byref(self.c))
         if nbytes == 0:
             raise MppiError(-1, self.lib.mppi_last_error().decode())
-        self._ws_raw = torch.empty(nbytes + 1024, dtype=torch.uint8, device=self.torch_device)
-        base = self._ws_raw.data_ptr()
+        # guard_bytes (test support): a patterned zone before and after the workspace, checked by guards_intact()
+        self._guard = guard_bytes
+        self._ws_raw = torch.empty(nbytes + 2048 + 2 * guard_bytes, dtype=torch.uint8, device=self.torch_device)
+        if guard_bytes:
+            self._ws_raw.fill_(0xA5)
+        base = self._ws_raw.data_ptr() + guard_bytes
         off = (-base) % 1024
         self.ws_ptr = base + off
+        self._ws_lo = guard_bytes + off
+        self._ws_hi = self._ws_lo + nbytes
         self.ctx = C.c_void_p()
         _lib._check(self.lib.mppi_create(C.byref(self.c), C.c_void_p(self.ws_ptr), nbytes, C.byref(self.ctx)))
         self.n, self.K, self.T = cfg.n_ctrl, cfg.K, cfg.T
@@ -61,6 +67,14 @@ class Controller:
         self.state_dim = 17 if getattr(cfg, "model", 0) == 1 else 10
         if debug_outputs:
             self.set_debug_outputs(True)
+
+    def guards_intact(self) -> bool:
+        """Test support (guard_bytes > 0): no kernel wrote into the patterned zones around the workspace."""
+        import torch
+        torch.cuda.synchronize(self.torch_device)
+        lo = self._ws_raw[self._ws_lo - self._guard:self._ws_lo]
+        hi = self._ws_raw[self._ws_hi:self._ws_hi + self._guard]
+        return bool((lo == 0xA5).all().item()) and bool((hi == 0xA5).all().item())
 
     def set_debug_outputs(self, on: bool):
         """Test support: also write s per query row in every step (debug("sdf")); off by default."""

@@ -280,3 +280,32 @@ def test_softmin_weights_and_mean_cost_diagnostics(name):
         np.testing.assert_allclose(d[b, 1], np.exp(-(J[b] - J[b].min()) / cfg.lam).sum(), rtol=1e-4)
         np.testing.assert_allclose(d[b, 2], 1.0 / (ref ** 2).sum(), rtol=1e-3)
         np.testing.assert_allclose(d[b, 3], J[b].mean(), rtol=1e-5)
+
+
+# ---------------------------------------------------------------- out-of-bounds writes (compute-sanitizer is closed)
+
+@pytest.mark.parametrize("name,over", [("c0", {}), ("c1s", {}), ("c2s", {}), ("c1pes", {}), ("c2pes", {}),
+                                       ("c4s", {"n_ctrl": 5, "K": 36, "T": 3}), ("c5s", {}), ("c1gs", {})])
+def test_no_writes_outside_the_workspace(name, over):
+    """Every kernel of the step (and the debug / sdf_eval paths) writes only inside the context's workspace:
+    64 KB patterned zones before and after it stay intact (ragged tiles, PE, the paper model, the analytic SDF)."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config(name, **over)
+    Ws, bs = synth.make_weights(cfg)
+    for mode in ("device", "external"):
+        c = Controller(cfg, noise_mode=mode, debug_outputs=True, guard_bytes=65536)
+        if cfg.sdf_provider == 0:
+            c.set_sdf_weights(Ws, bs)
+        c.set_latent(synth.make_latents(cfg), synth.make_query_transforms(cfg))
+        c.set_nominal(synth.make_nominal(cfg))
+        if mode == "external":
+            c.set_noise(synth.make_noise(cfg))
+        for step in range(3):
+            c.step(synth.make_x0(cfg), synth.make_goals(cfg), step)
+        c.get_controls(allow_nonfinite=True)
+        for what in ("queries", "sdf", "costs", "terms", "partial", "weights"):
+            c.debug(what)
+        if cfg.sdf_provider == 0:
+            c.sdf_eval(synth.make_query_rows(131, seed=4)).cpu()
+        assert c.guards_intact(), (name, mode)
+        c.close()
