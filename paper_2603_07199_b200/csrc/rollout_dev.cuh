@@ -24,6 +24,12 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 
 __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
 
+__device__ __forceinline__ float sqrt_approx(float v) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
 // Standard normals of (global sample g, step t, iteration step): Philox4x32-10 (key = seed, counter =
 // (g, t, step_lo, step_hi)), u = ((x >> 9) + 0.5) 2^-23, Box-Muller on (u0,u1), (u2,u3) (reading R24').
 __device__ __forceinline__ float4 philox_normals(unsigned long long g, int t, unsigned long long step,
@@ -33,9 +39,9 @@ __device__ __forceinline__ float4 philox_normals(unsigned long long g, int t, un
     const float s23 = 1.1920928955078125e-07f;  // 2^-23
     const float u0 = ((float)(c[0] >> 9) + 0.5f) * s23, u1 = ((float)(c[1] >> 9) + 0.5f) * s23;
     const float u2 = ((float)(c[2] >> 9) + 0.5f) * s23, u3 = ((float)(c[3] >> 9) + 0.5f) * s23;
-    // fast SFU forms (MUFU.LG2 / SIN / COS, abs error ~2^-21 on these ranges):
+    // fast SFU forms (MUFU.LG2 / SQRT / SIN / COS, abs error ~2^-21 on these ranges):
     // cos(2 pi u) = -cos(theta), sin(2 pi u) = -sin(theta), theta = 2 pi (u - 1/2) in [-pi, pi)
-    const float r0 = sqrtf(-2.f * __logf(u0)), r1 = sqrtf(-2.f * __logf(u2));
+    const float r0 = sqrt_approx(-2.f * __logf(u0)), r1 = sqrt_approx(-2.f * __logf(u2));
     float s0, c0, s1, c1;
     __sincosf(6.283185307179586f * (u1 - 0.5f), &s0, &c0);
     __sincosf(6.283185307179586f * (u3 - 0.5f), &s1, &c1);
@@ -50,63 +56,95 @@ __device__ __forceinline__ unsigned long long global_sample(const Params& p, int
            (unsigned long long)k;
 }
 
-// CTBR dynamics xdot = f(x, u): x = [p, v, q(w,x,y,z)], com = c/m, body rates (wx, wy, wz).
-__device__ __forceinline__ void dyn_ctbr(const float* x, float com, float wx, float wy, float wz, float g, float* xd) {
-    const float qw = x[6], qx = x[7], qy = x[8], qz = x[9];
-    xd[0] = x[3]; xd[1] = x[4]; xd[2] = x[5];
-    xd[3] = com * (2.f * (qx * qz + qw * qy));
-    xd[4] = com * (2.f * (qy * qz - qw * qx));
-    xd[5] = com * (1.f - 2.f * (qx * qx + qy * qy)) - g;
-    xd[6] = 0.5f * (-qx * wx - qy * wy - qz * wz);
-    xd[7] = 0.5f * (qw * wx + qy * wz - qz * wy);
-    xd[8] = 0.5f * (qw * wy + qz * wx - qx * wz);
-    xd[9] = 0.5f * (qw * wz + qx * wy - qy * wx);
-}
-
-
 // One CTBR rollout step of one sample (readings R4, R5, R7, R11, R12): the clamped
 // input u = clamp(U*_t + sigma n), classic RK4 with u held, q renormalised; then the query rows of x_{t+1}
 // in the cached frame (p_c = R p + t_q, |v|) and (p_c + h v_c/|v|, 0), and the non-SDF
-// stage cost w_goal |p - g_c|^2 + w_u |u|^2 added to part. Shared by k_rollout and the fused rollout producer
-// of kernel_mlp_h128.cu, so both produce the same rows.
+// stage cost w_goal |p - g_c|^2 + w_u |u|^2 added to part. Shared by k_rollout and the fused rollout producers
+// of the SDF-MLP kernels, so all produce the same rows.
+// Issue-bound at configs[3..4] (one thread per sample, T dependent steps): the state updates run as f32x2
+// pairs (FFMA2 / FADD2 on (px,py), (vx,vy), (qw,qx), (qy,qz); pz and vz scalar), the quaternion rates use the
+// half body rates, |v| is MUFU.SQRT (sqrt.approx, ~1 ulp) -- about 200 instructions per step instead of ~300.
+// xdot for the pair layout: a = (ax, ay), az, dq01 = (qw', qx'), dq23 = (qy', qz'); hw = half body rates
+__device__ __forceinline__ void dyn_ctbr2(float2 q01, float2 q23, float com2, float comg, float hwx, float hwy,
+                                         float hwz, float2& a, float& az, float2& dq01, float2& dq23) {
+    const float qw = q01.x, qx = q01.y, qy = q23.x, qz = q23.y;
+    a.x = com2 * fmaf(qx, qz, qw * qy);
+    a.y = com2 * fmaf(qy, qz, -qw * qx);
+    az = fmaf(-com2, fmaf(qx, qx, qy * qy), comg);       // (c/m)(1 - 2(qx^2 + qy^2)) - g
+    dq01.x = fmaf(-qx, hwx, fmaf(-qy, hwy, -qz * hwz));
+    dq01.y = fmaf(qw, hwx, fmaf(qy, hwz, -qz * hwy));
+    dq23.x = fmaf(qw, hwy, fmaf(qz, hwx, -qx * hwz));
+    dq23.y = fmaf(qw, hwz, fmaf(qx, hwy, -qy * hwx));
+}
+
 __device__ __forceinline__ void ctbr_step(const Params& p, float (&x)[10], float4 U, float4 n, const float (&R)[9],
                                           const float (&tq)[3], const float (&gc)[3], float inv_mass, float4& row0,
                                           float4& row1, float& part) {
-    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt / 6.f, g = p.gravity;
-    const float u0 = clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]);
-    const float u1 = clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]);
-    const float u2 = clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]);
-    const float u3 = clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]);
-    const float com = u0 * inv_mass;
-    float k1[10], k2[10], k3[10], k4[10], xt[10];
-    dyn_ctbr(x, com, u1, u2, u3, g, k1);
-#pragma unroll
-    for (int i = 0; i < 10; ++i) xt[i] = x[i] + hdt * k1[i];
-    dyn_ctbr(xt, com, u1, u2, u3, g, k2);
-#pragma unroll
-    for (int i = 0; i < 10; ++i) xt[i] = x[i] + hdt * k2[i];
-    dyn_ctbr(xt, com, u1, u2, u3, g, k3);
-#pragma unroll
-    for (int i = 0; i < 10; ++i) xt[i] = x[i] + dt * k3[i];
-    dyn_ctbr(xt, com, u1, u2, u3, g, k4);
-#pragma unroll
-    for (int i = 0; i < 10; ++i) x[i] = x[i] + dt6 * (k1[i] + 2.f * k2[i] + 2.f * k3[i] + k4[i]);
-    const float qinv = rsqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);   // MUFU, ~2 ulp
-#pragma unroll
-    for (int i = 6; i < 10; ++i) x[i] = x[i] * qinv;
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.f / 6.f), g = p.gravity;
+    const float u0 = clampf(fmaf(p.sigma[0], n.x, U.x), p.u_lo[0], p.u_hi[0]);
+    const float u1 = clampf(fmaf(p.sigma[1], n.y, U.y), p.u_lo[1], p.u_hi[1]);
+    const float u2 = clampf(fmaf(p.sigma[2], n.z, U.z), p.u_lo[2], p.u_hi[2]);
+    const float u3 = clampf(fmaf(p.sigma[3], n.w, U.w), p.u_lo[3], p.u_hi[3]);
+    const float com = u0 * inv_mass, com2 = 2.f * com, comg = com - g;
+    const float hwx = 0.5f * u1, hwy = 0.5f * u2, hwz = 0.5f * u3;
+    const float2 P = make_float2(x[0], x[1]), V = make_float2(x[3], x[4]);
+    const float pz = x[2], vz = x[5];
+    const float2 Q01 = make_float2(x[6], x[7]), Q23 = make_float2(x[8], x[9]);
+    const float2 H2 = make_float2(hdt, hdt), D2 = make_float2(dt, dt);
+    // stage 1 (k1: dP = V, dpz = vz)
+    float2 a1, dq01_1, dq23_1;
+    float az1;
+    dyn_ctbr2(Q01, Q23, com2, comg, hwx, hwy, hwz, a1, az1, dq01_1, dq23_1);
+    // stage 2 at x + hdt k1
+    const float2 V2 = __ffma2_rn(H2, a1, V);
+    const float vz2 = fmaf(hdt, az1, vz);
+    float2 a2, dq01_2, dq23_2;
+    float az2;
+    dyn_ctbr2(__ffma2_rn(H2, dq01_1, Q01), __ffma2_rn(H2, dq23_1, Q23), com2, comg, hwx, hwy, hwz, a2, az2, dq01_2,
+              dq23_2);
+    // stage 3 at x + hdt k2
+    const float2 V3 = __ffma2_rn(H2, a2, V);
+    const float vz3 = fmaf(hdt, az2, vz);
+    float2 a3, dq01_3, dq23_3;
+    float az3;
+    dyn_ctbr2(__ffma2_rn(H2, dq01_2, Q01), __ffma2_rn(H2, dq23_2, Q23), com2, comg, hwx, hwy, hwz, a3, az3, dq01_3,
+              dq23_3);
+    // stage 4 at x + dt k3
+    const float2 V4 = __ffma2_rn(D2, a3, V);
+    const float vz4 = fmaf(dt, az3, vz);
+    float2 a4, dq01_4, dq23_4;
+    float az4;
+    dyn_ctbr2(__ffma2_rn(D2, dq01_3, Q01), __ffma2_rn(D2, dq23_3, Q23), com2, comg, hwx, hwy, hwz, a4, az4, dq01_4,
+              dq23_4);
+    // x + dt/6 (k1 + 2 k2 + 2 k3 + k4); the position rates k_i are the stage velocities V, V2, V3, V4
+    const float2 T2 = make_float2(2.f, 2.f), S6 = make_float2(dt6, dt6);
+    const float2 sP = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(V2, V3), V), V4);
+    const float2 sV = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(a2, a3), a1), a4);
+    const float2 s01 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(dq01_2, dq01_3), dq01_1), dq01_4);
+    const float2 s23 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(dq23_2, dq23_3), dq23_1), dq23_4);
+    const float2 Pn = __ffma2_rn(S6, sP, P), Vn = __ffma2_rn(S6, sV, V);
+    const float pzn = fmaf(dt6, fmaf(2.f, vz2 + vz3, vz) + vz4, pz);
+    const float vzn = fmaf(dt6, fmaf(2.f, az2 + az3, az1) + az4, vz);
+    float2 q01 = __ffma2_rn(S6, s01, Q01), q23 = __ffma2_rn(S6, s23, Q23);
+    const float qinv = rsqrtf(fmaf(q01.x, q01.x, fmaf(q01.y, q01.y, fmaf(q23.x, q23.x, q23.y * q23.y))));  // MUFU
+    const float2 QI = make_float2(qinv, qinv);
+    q01 = __fmul2_rn(q01, QI);
+    q23 = __fmul2_rn(q23, QI);
+    x[0] = Pn.x; x[1] = Pn.y; x[2] = pzn; x[3] = Vn.x; x[4] = Vn.y; x[5] = vzn;
+    x[6] = q01.x; x[7] = q01.y; x[8] = q23.x; x[9] = q23.y;
     // query-frame position and direction, scored at x_{t+1} (reading R7)
     float pc[3], dv[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        pc[r] = R[3 * r] * x[0] + R[3 * r + 1] * x[1] + R[3 * r + 2] * x[2] + tq[r];
-        dv[r] = R[3 * r] * x[3] + R[3 * r + 1] * x[4] + R[3 * r + 2] * x[5];
+        pc[r] = fmaf(R[3 * r], x[0], fmaf(R[3 * r + 1], x[1], fmaf(R[3 * r + 2], x[2], tq[r])));
+        dv[r] = fmaf(R[3 * r], x[3], fmaf(R[3 * r + 1], x[4], R[3 * r + 2] * x[5]));
     }
-    const float nv = sqrtf(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+    const float nv = sqrt_approx(fmaf(x[3], x[3], fmaf(x[4], x[4], x[5] * x[5])));
     const float sc = nv >= 1e-6f ? __fdividef(p.fd_h, nv) : 0.f;
     row0 = make_float4(pc[0], pc[1], pc[2], nv);
-    row1 = make_float4(pc[0] + sc * dv[0], pc[1] + sc * dv[1], pc[2] + sc * dv[2], 0.f);
+    row1 = make_float4(fmaf(sc, dv[0], pc[0]), fmaf(sc, dv[1], pc[1]), fmaf(sc, dv[2], pc[2]), 0.f);
     const float dx = x[0] - gc[0], dy = x[1] - gc[1], dz = x[2] - gc[2];
-    part += p.w_goal * (dx * dx + dy * dy + dz * dz) + p.w_u * (u0 * u0 + u1 * u1 + u2 * u2 + u3 * u3);
+    part += p.w_goal * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) + p.w_u * fmaf(u0, u0, fmaf(u1, u1, fmaf(u2, u2, u3 * u3)));
 }
 
 }  // namespace mppi
