@@ -45,9 +45,25 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, extra
     # one nvcc per translation unit, in parallel (the two tensor-core kernels dominate), then one link
     objs = [f"{tmp}.{os.path.basename(src)}.o" for src in sources()]
 
+    # per-TU object cache (local builds only): key = the TU, every header it can include, the flags
+    import hashlib, shutil
+    cache = os.environ.get("MPPI_OBJ_CACHE", "/tmp/mppi_objcache")
+    hdrs = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "mppi.h")]
+    hdr_hash = hashlib.sha256(b"".join(open(h, "rb").read() for h in hdrs) + " ".join(flags).encode()).hexdigest()
+
     def compile_one(src_obj):
         src, obj = src_obj
-        return subprocess.run([nvcc, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+        key = hashlib.sha256(open(src, "rb").read() + hdr_hash.encode()).hexdigest()[:24]
+        cached = os.path.join(cache, f"{os.path.basename(src)}.{key}.o")
+        if os.path.exists(cached) and not verbose:
+            shutil.copyfile(cached, obj)
+            return subprocess.CompletedProcess([], 0, "", "")
+        r = subprocess.run([nvcc, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+        if r.returncode == 0:
+            os.makedirs(cache, exist_ok=True)
+            shutil.copyfile(obj, cached + f".{os.getpid()}")
+            os.replace(cached + f".{os.getpid()}", cached)
+        return r
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=len(objs)) as ex:
         results = list(ex.map(compile_one, zip(sources(), objs)))

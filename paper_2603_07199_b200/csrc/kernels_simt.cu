@@ -93,7 +93,10 @@ __device__ void rollout_noise_producer(const Params& p, const Buffers& b, int bb
 constexpr int kMaxTStaged = 128;   // nominal staged in shared memory up to this horizon
 
 template <bool DEV>
-__global__ void __launch_bounds__(2 * kRolloutBlock) k_rollout(Params p, Buffers b) {
+#ifndef MPPI_RO_MINB
+#define MPPI_RO_MINB 7   // resident rollout blocks per SM: 72 registers (measured r02: 6 -> 7 raises issue-active)
+#endif
+__global__ void __launch_bounds__(2 * kRolloutBlock, MPPI_RO_MINB) k_rollout(Params p, Buffers b) {
     __shared__ float4 s_n[2][kRolloutBlock];   // DEV: normals of steps t (read) and t + 1 (being written)
     __shared__ float4 s_U[kMaxTStaged];   // the shifted nominal U*_t of this controller (L1-latency reads)
     const int bb = blockIdx.y;
@@ -387,6 +390,9 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 constexpr int kSoftminThreads = 512;   // 512/SPB threads per sample in phase 1, 16 warps over t in phase 2
 // samples per block: 256, or 512 from K = 65536 on (configs[3]: 256 blocks, one wave at 2 blocks per SM)
 __host__ __device__ constexpr int softmin_spb(int K) { return K >= 65536 ? 512 : 256; }
+// two-level record combine from 33 sample blocks on: groups of kSoftminGroup (0 = one level)
+constexpr int kSoftminGroup = 16;
+__host__ __device__ constexpr int softmin_groups(int nblk) { return nblk > 32 ? (nblk + kSoftminGroup - 1) / kSoftminGroup : 0; }
 
 __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) {
     #pragma unroll
@@ -403,12 +409,162 @@ __device__ __forceinline__ float block_reduce(float v, float* red, bool is_min) 
     return r;
 }
 
+#ifdef MPPI_TC_TRACE
+// Debug-only timeline of k_softmin (controller 0, T slice 0, first 1024 blocks): %globaltimer at block start,
+// after phase 1, after the reductions, after phase 2, after the combine (last block only), and the SM id
+__device__ unsigned long long g_sm_trace[1024][10];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SM_TRACE(i)                                                                                    \
+    do {                                                                                               \
+        if (blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 1024 && threadIdx.x == 0) {             \
+            g_sm_trace[blockIdx.x][i] = gtimer();                                                      \
+            if ((i) == 0) { unsigned s_; asm("mov.u32 %0, %%smid;" : "=r"(s_)); g_sm_trace[blockIdx.x][5] = s_; } \
+        }                                                                                              \
+    } while (0)
+int softmin_trace_copy(unsigned long long* host, int max_entries) {
+    const int n = max_entries < 1024 * 10 ? max_entries : 1024 * 10;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host, g_sm_trace, (size_t)n * 8);
+    return n;
+}
+#else
+#define SM_TRACE(i) do {} while (0)
+int softmin_trace_copy(unsigned long long*, int) { return 0; }
+#endif
+
+// four sums with the tree of block_reduce per component (same results as four block_reduce calls)
+__device__ __forceinline__ float4 block_reduce4(float4 v, float4* red4) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xFFFFFFFFu, v.x, o);
+        v.y += __shfl_xor_sync(0xFFFFFFFFu, v.y, o);
+        v.z += __shfl_xor_sync(0xFFFFFFFFu, v.z, o);
+        v.w += __shfl_xor_sync(0xFFFFFFFFu, v.w, o);
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red4[w] = v;
+    __syncthreads();
+    float4 r = red4[0];
+    for (int i = 1; i < nw; ++i) {
+        const float4 q = red4[i];
+        r.x += q.x; r.y += q.y; r.z += q.z; r.w += q.w;
+    }
+    return r;
+}
+
+// Record combine of k_softmin (the softmin shard-combine identity; records in order): m = min m_b,
+// f_b = exp((m - m_b)/lambda), S = sum S_b f_b, S2 = sum S2_b f_b^2, V = sum V_b f_b; final: U* = U + V/S (or this
+// rank's record) and the diagnostics, else the group record out_rec. It runs once per step on one SM, so its code
+// is cold in the instruction caches (trace build: ~5 us per phase of an unrolled, thrice-inlined form whatever
+// the record count); hence one out-of-line copy (the final level runs right after the same SM's group level, so
+// warm) of short rolled loops: record heads staged in shared memory (one record per thread), per-thread sums.
+struct CombineOut {   // by value: a reference to the kernel's Params would copy them to every thread's stack
+    int T, bb, W;
+    float inv_lambda;
+    float* record;
+    const float* U_nom;
+    float* U_out;
+    float* diag;
+    int* flags;
+};
+__device__ __noinline__ void softmin_combine(const CombineOut o, const float* recs, int n, bool final_level,
+                                             float* out_rec, int write_record, float (*s_hd)[kSoftminThreads],
+                                             float* s_f) {
+    const int W = o.W, bb = o.bb;
+    const int nh = min(n, kSoftminThreads);
+    if (threadIdx.x < nh) {
+        const float* r = recs + (long long)threadIdx.x * W;
+        const float h0 = __ldcg(r), h1 = __ldcg(r + 1), h2 = __ldcg(r + 2), h3 = __ldcg(r + 3), h4 = __ldcg(r + 4);
+        s_hd[0][threadIdx.x] = h0; s_hd[1][threadIdx.x] = h1; s_hd[2][threadIdx.x] = h2;
+        s_hd[3][threadIdx.x] = h3; s_hd[4][threadIdx.x] = h4;
+    }
+    __syncthreads();
+    float mg = INFINITY;
+#pragma unroll 1
+    for (int i = 0; i < nh; ++i) mg = fminf(mg, s_hd[0][i]);
+#pragma unroll 1
+    for (int i = nh; i < n; ++i) mg = fminf(mg, __ldcg(recs + (long long)i * W));
+    const bool ok = mg < INFINITY;
+    if (threadIdx.x < nh) {
+        const float mi = s_hd[0][threadIdx.x];
+        s_f[threadIdx.x] = (ok && mi < INFINITY) ? expf((mg - mi) * o.inv_lambda) : 0.f;
+    }
+    __syncthreads();
+    auto fscale_far = [&](int i) {   // records past the first 512
+        const float mi = __ldcg(recs + (long long)i * W);
+        return (ok && mi < INFINITY) ? expf((mg - mi) * o.inv_lambda) : 0.f;
+    };
+    float Sg = 0.f, S2g = 0.f, SJg = 0.f, NJg = 0.f;
+#pragma unroll 1
+    for (int i = 0; i < nh; ++i) {
+        const float f = s_f[i];
+        Sg = fmaf(s_hd[1][i], f, Sg);
+        S2g = fmaf(s_hd[2][i] * f, f, S2g);
+        SJg += s_hd[3][i];
+        NJg += s_hd[4][i];
+    }
+#pragma unroll 1
+    for (int i = nh; i < n; ++i) {
+        const float f = fscale_far(i);
+        const float* r = recs + (long long)i * W;
+        Sg = fmaf(__ldcg(r + 1), f, Sg);
+        S2g = fmaf(__ldcg(r + 2) * f, f, S2g);
+        SJg += __ldcg(r + 3);
+        NJg += __ldcg(r + 4);
+    }
+#pragma unroll 1
+    for (int tc = threadIdx.x; tc < 4 * o.T; tc += blockDim.x) {
+        float V = 0.f;
+        if (ok) {
+#pragma unroll 8
+            for (int i = 0; i < nh; ++i) V = fmaf(__ldcg(recs + (long long)i * W + kRecHead + tc), s_f[i], V);
+#pragma unroll 1
+            for (int i = nh; i < n; ++i) V = fmaf(__ldcg(recs + (long long)i * W + kRecHead + tc), fscale_far(i), V);
+        }
+        const int t = tc >> 2, c = tc & 3;
+        if (!final_level) {
+            out_rec[kRecHead + tc] = V;
+        } else if (write_record) {
+            o.record[(long long)bb * W + kRecHead + tc] = V;
+        } else {
+            const float Uv = o.U_nom[((long long)bb * o.T + t) * 4 + c];
+            o.U_out[((long long)bb * o.T + t) * 4 + c] = (ok && Sg > 0.f) ? Uv + V / Sg : Uv;
+        }
+    }
+    if (threadIdx.x == 0) {
+        float* out = !final_level ? out_rec : write_record ? o.record + (long long)bb * W : nullptr;
+        if (out) {
+            out[0] = mg; out[1] = Sg; out[2] = S2g; out[3] = SJg;
+            out[4] = NJg; out[5] = out[6] = out[7] = 0.f;
+        } else {
+            float* d = o.diag + bb * 4;
+            d[0] = mg;
+            d[1] = Sg;
+            d[2] = S2g > 0.f ? Sg * Sg / S2g : 0.f;
+            d[3] = NJg > 0.f ? SJg / NJg : INFINITY;
+            o.flags[bb] = ok ? 0 : 1;
+        }
+    }
+}
+
+// resident blocks per SM: 256-sample blocks two (64 registers), 512-sample blocks one
 template <int kSoftminBlock>
-__global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b, int write_record) {
-    constexpr int TPS = kSoftminThreads / kSoftminBlock;   // threads per sample in phase 1 (1 or 2)
+__host__ __device__ constexpr int kSoftminMinBlocks() { return kSoftminBlock == 256 ? 2 : 1; }
+
+template <int kSoftminBlock>
+__global__ void __launch_bounds__(kSoftminThreads, kSoftminMinBlocks<kSoftminBlock>()) k_softmin(Params p, Buffers b, int write_record) {
     __shared__ float s_w[kSoftminBlock];
-    __shared__ float s_half[kSoftminBlock];
+    // phase 1 partition: a thread sums the terms of 4 consecutive samples (float4 loads, 16 in flight: 256 B per
+    // thread, enough bytes in flight per SM to stream the terms at HBM rate) over one of NSL time slices
+    constexpr int QB = kSoftminBlock / 4, NSL = kSoftminThreads / QB;
+    __shared__ float s_part[NSL][kSoftminBlock];
     __shared__ float red[kSoftminThreads / 32];
+    __shared__ float4 red4[kSoftminThreads / 32];
     __shared__ bool s_last;
     // grid (sample blocks, controllers, T slices): every T slice recomputes the sample block's J, m, S
     // (identically) and accumulates V only over its own time steps, so the noise-bound phase 2 runs on
@@ -417,149 +573,196 @@ __global__ void __launch_bounds__(kSoftminThreads) k_softmin(Params p, Buffers b
     const int kk = threadIdx.x % kSoftminBlock, half = threadIdx.x / kSoftminBlock;
     const int k = blockIdx.x * kSoftminBlock + kk;
     const int W = kRecHead + 4 * p.T;   // m, S, S2, SJ, N, pad x3, V[T][4] (16-B aligned)
-    // ---- phase 1: two threads per sample, each summing half of the horizon's terms in t order
+    // ---- phase 1: J_k = partial_k + sum over the NSL slices (in order) of each slice's terms summed in t order
+    SM_TRACE(0);
     float J = INFINITY;
     {
-        const int th = (p.T + TPS - 1) / TPS, t0 = half * th, t1 = min(p.T, t0 + th);
-        float acc = 0.f;
-        if (k < p.K) {
-            const float* tp = b.terms + (long long)bb * p.T * p.K + k;
-            // streamed once; 16 independent loads in flight per thread
-            int t = t0;
-            for (; t + 16 <= t1; t += 16) {
-                float v[16];
+        const int q = threadIdx.x % QB, sl = threadIdx.x / QB;
+        const int kq = blockIdx.x * kSoftminBlock + 4 * q;
+        const int th = (p.T + NSL - 1) / NSL, t0 = sl * th, t1 = min(p.T, t0 + th);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kq < p.K) {
+            const float* tp = b.terms + (long long)bb * p.T * p.K + kq;
+            if ((p.K & 3) == 0) {   // 16-B aligned quads (every config; ragged K takes the scalar form)
+                const long long st4 = p.K / 4;
+                const float4* tp4 = reinterpret_cast<const float4*>(tp);
+                constexpr int PB = kSoftminMinBlocks<kSoftminBlock>() == 2 ? 8 : 16;   // loads in flight (64 registers: 8)
+                int t = t0;
+                for (; t + PB <= t1; t += PB) {
+                    float4 v[PB];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = __ldcs(tp + (long long)(t + i) * p.K);
+                    for (int i = 0; i < PB; ++i) v[i] = __ldcs(tp4 + (long long)(t + i) * st4);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) acc += v[i];
+                    for (int i = 0; i < PB; ++i) {
+                        acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
+                    }
+                }
+                for (; t < t1; ++t) {
+                    const float4 v = __ldcs(tp4 + (long long)t * st4);
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                }
+            } else {
+                const int nq = min(4, p.K - kq);
+                for (int t = t0; t < t1; ++t) {
+                    const float* r = tp + (long long)t * p.K;
+                    acc.x += __ldcs(r);
+                    if (nq > 1) acc.y += __ldcs(r + 1);
+                    if (nq > 2) acc.z += __ldcs(r + 2);
+                    if (nq > 3) acc.w += __ldcs(r + 3);
+                }
             }
-            for (; t < t1; ++t) acc += __ldcs(tp + (long long)t * p.K);
         }
-        if (TPS > 1 && half == 1) s_half[kk] = acc;
+        *reinterpret_cast<float4*>(&s_part[sl][4 * q]) = acc;
         __syncthreads();
         if (half == 0 && k < p.K) {
-            acc = b.partial[(long long)bb * p.K + k] + acc + (TPS > 1 ? s_half[kk] : 0.f);
-            J = isfinite(acc) ? acc : INFINITY;
+            float tsum = s_part[0][kk];
+#pragma unroll
+            for (int i = 1; i < NSL; ++i) tsum += s_part[i][kk];
+            const float a = b.partial[(long long)bb * p.K + k] + tsum;
+            J = isfinite(a) ? a : INFINITY;
             if (tz == 0) b.J[(long long)bb * p.K + k] = J;
         }
     }
+    SM_TRACE(1);
     const float m = block_reduce(J, red, true);
     const float w = (J < INFINITY) ? expf((m - J) * p.inv_lambda) : 0.f;   // 0 for the second half
     if (half == 0) s_w[kk] = w;
-    const float S = block_reduce(w, red, false);
-    const float S2 = block_reduce(w * w, red, false);
+    // S, S2 and the mean-cost diagnostic (sum and count of the finite costs) in one reduction
+    const float4 sums = block_reduce4(make_float4(w, w * w, J < INFINITY ? J : 0.f, J < INFINITY ? 1.f : 0.f), red4);
+    const float S = sums.x;
     float* rec = b.blkrec + ((long long)bb * nblk + blockIdx.x) * W;
-    if (tz == 0) {   // mean-cost diagnostic: sum and count of the finite costs
-        const float SJ = block_reduce(J < INFINITY ? J : 0.f, red, false);
-        const float NJ = block_reduce(J < INFINITY ? 1.f : 0.f, red, false);
-        if (threadIdx.x == 0) {
-            rec[0] = m; rec[1] = S; rec[2] = S2; rec[3] = SJ;
-            rec[4] = NJ; rec[5] = rec[6] = rec[7] = 0.f;
-        }
+    if (tz == 0 && threadIdx.x == 0) {
+        rec[0] = m; rec[1] = S; rec[2] = sums.y; rec[3] = sums.z;
+        rec[4] = sums.w; rec[5] = rec[6] = rec[7] = 0.f;
     }
     // ---- phase 2: warp per time step (coalesced over the block's samples), fixed shuffle tree
     const int kn = min(kSoftminBlock, p.K - (int)blockIdx.x * kSoftminBlock);
     const long long NK = (long long)p.n_ctrl * p.K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int tsl = (p.T + nz_t - 1) / nz_t, tb = tz * tsl, te = min(p.T, tb + tsl);
-    for (int t = tb + warp; t < te; t += nw) {
-        const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+    SM_TRACE(2);
+    // this lane's softmin weights (samples lane + 32 r) in registers for every t of the warp
+    constexpr int PER = kSoftminBlock / 32;
+    float wr[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int i = lane + 32 * r;
+        wr[r] = i < kn ? s_w[i] : 0.f;
+    }
+    // V[t] partial of one half (PH float4 per lane) of the block's samples, in sample order
+    // parts per t: 512-sample blocks (one block per SM): 2 x 8 float4, each part's loads in flight while the
+    // previous part is summed (measured configs[3]: the same time at two blocks per SM with 4 x 4); 256-sample
+    // blocks (two per SM, 64 registers): one part of 8 (the ping-pong form spills there: configs[4] 0.20 -> 0.23 ms)
+    constexpr int PH = 8, NH = PER / PH;
+    auto v_load = [&](int t, int h, float4 (&nv)[PH]) {
         const float4* nz = b.noise + (long long)t * NK + (long long)bb * p.K + (long long)blockIdx.x * kSoftminBlock;
-        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-        if (m < INFINITY) {
-            // all of this lane's noise loads for step t first (kSoftminBlock / 32 in flight), then the sums in
-            // sample order (the loads interleaved with the FMA chains ran at ~0.5 TB/s)
-            constexpr int PER = kSoftminBlock / 32;
-            float4 nv[PER];
 #pragma unroll
-            for (int r = 0; r < PER; ++r) {
-                const int i = lane + 32 * r;
-                nv[r] = i < kn ? __ldcs(nz + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+        for (int r = 0; r < PH; ++r) {
+            const int i = lane + 32 * (h * PH + r);
+            nv[r] = i < kn ? __ldcs(nz + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto v_acc = [&](const float4& U, int h, const float4 (&nv)[PH], float4& v) {
 #pragma unroll
-            for (int r = 0; r < PER; ++r) {
-                const int i = lane + 32 * r;
-                if (i < kn) {
-                    const float wi = s_w[i];
-                    const float4 n = nv[r];
-                    v0 = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v0);
-                    v1 = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v1);
-                    v2 = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v2);
-                    v3 = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v3);
-                }
+        for (int r = 0; r < PH; ++r) {
+            const int i = lane + 32 * (h * PH + r);
+            if (i < kn) {
+                const float wi = wr[h * PH + r];
+                const float4 n = nv[r];
+                v.x = fmaf(wi, clampf(U.x + p.sigma[0] * n.x, p.u_lo[0], p.u_hi[0]) - U.x, v.x);
+                v.y = fmaf(wi, clampf(U.y + p.sigma[1] * n.y, p.u_lo[1], p.u_hi[1]) - U.y, v.y);
+                v.z = fmaf(wi, clampf(U.z + p.sigma[2] * n.z, p.u_lo[2], p.u_hi[2]) - U.z, v.z);
+                v.w = fmaf(wi, clampf(U.w + p.sigma[3] * n.w, p.u_lo[3], p.u_hi[3]) - U.w, v.w);
             }
         }
+    };
+    auto v_store = [&](int t, float4 v) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            v0 += __shfl_xor_sync(0xFFFFFFFFu, v0, o);
-            v1 += __shfl_xor_sync(0xFFFFFFFFu, v1, o);
-            v2 += __shfl_xor_sync(0xFFFFFFFFu, v2, o);
-            v3 += __shfl_xor_sync(0xFFFFFFFFu, v3, o);
+            v.x += __shfl_xor_sync(0xFFFFFFFFu, v.x, o);
+            v.y += __shfl_xor_sync(0xFFFFFFFFu, v.y, o);
+            v.z += __shfl_xor_sync(0xFFFFFFFFu, v.z, o);
+            v.w += __shfl_xor_sync(0xFFFFFFFFu, v.w, o);
         }
-        if (lane == 0) reinterpret_cast<float4*>(rec + kRecHead)[t] = make_float4(v0, v1, v2, v3);
+        if (lane == 0) reinterpret_cast<float4*>(rec + kRecHead)[t] = v;
+    };
+    const bool live = m < INFINITY;
+    if constexpr (NH == 1) {
+        for (int t = tb + warp; t < te; t += nw) {
+            const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live) {   // all of this lane's loads for step t first, then the sums in sample order
+                float4 nv[PH];
+                v_load(t, 0, nv);
+                v_acc(U, 0, nv, v);
+            }
+            v_store(t, v);
+        }
+    } else {
+        static_assert(NH % 2 == 0, "ping-pong over an even number of parts");
+        float4 A[PH], B[PH];
+        int t = tb + warp;
+        if (live && t < te) v_load(t, 0, A);
+        for (; t < te; t += nw) {
+            const float4 U = reinterpret_cast<const float4*>(b.U_nom)[(long long)bb * p.T + t];
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    float4(&cur)[PH] = (h & 1) ? B : A;
+                    float4(&nxt)[PH] = (h & 1) ? A : B;
+                    if (h + 1 < NH) v_load(t, h + 1, nxt);
+                    else if (t + nw < te) v_load(t + nw, 0, nxt);
+                    v_acc(U, h, cur, v);
+                }
+            }
+            v_store(t, v);
+        }
     }
-    // ---- last block of this controller combines the block records in order
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(b.tickets + bb, 1u) == (unsigned)(nblk * nz_t - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const float* recs = b.blkrec + (long long)bb * nblk * W;
-    __shared__ float s_f[kSoftminThreads];   // per-record scale exp((m - m_b)/lambda), nblk <= blocks handled below
-    // global min over block records (thread i reads record i; tree with fixed shape)
-    float mi_loc = INFINITY;
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) mi_loc = fminf(mi_loc, __ldcg(recs + (long long)i * W));
-    const float mg = block_reduce(mi_loc, red, true);
-    const bool ok = mg < INFINITY;
-    float sl = 0.f, s2l = 0.f, sjl = 0.f, njl = 0.f;
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
-        const float* r = recs + (long long)i * W;
-        const float mi = __ldcg(r);
-        const float f = (ok && mi < INFINITY) ? expf((mg - mi) * p.inv_lambda) : 0.f;
-        if (i < kSoftminThreads) s_f[i] = f;
-        sl += __ldcg(r + 1) * f;
-        s2l += __ldcg(r + 2) * f * f;
-        sjl += __ldcg(r + 3);
-        njl += __ldcg(r + 4);
-    }
-    const float Sg = block_reduce(sl, red, false);
-    const float S2g = block_reduce(s2l, red, false);
-    const float SJg = block_reduce(sjl, red, false);
-    const float NJg = block_reduce(njl, red, false);
-    for (int tc = threadIdx.x; tc < 4 * p.T; tc += blockDim.x) {
-        float V = 0.f;
-        if (ok) {
-#pragma unroll 16
-            for (int i = 0; i < nblk; ++i) {
-                const float f = i < kSoftminThreads ? s_f[i]
-                                                  : expf((mg - __ldcg(recs + (long long)i * W)) * p.inv_lambda);
-                V = fmaf(__ldcg(recs + (long long)i * W + kRecHead + tc), f, V);
+    SM_TRACE(3);
+    // ---- combine the block records in order (the softmin shard-combine identity, so the result is exact up to
+    // rounding and deterministic): m = min m_b, f_b = exp((m - m_b)/lambda), S = sum S_b f_b, V = sum V_b f_b.
+    // Up to 32 sample blocks: the last block of the controller (atomic ticket) combines them all. More (configs[3]:
+    // 256): two levels -- the last block of each group of kSoftminGroup sample blocks combines the group into a
+    // group record, the last group combiner combines the group records -- so the single-SM tail reads
+    // kSoftminGroup + n_groups records instead of nblk (measured configs[3]: 18 us of a 69 us kernel flat).
+    __shared__ float s_hd[5][kSoftminThreads];   // record heads of a combine (softmin_combine)
+    __shared__ float s_f[kSoftminThreads];
+    auto combine = [&](const float* recs, int n, bool final_level, float* out_rec) {
+        const CombineOut o{p.T, bb, W, p.inv_lambda, b.record, b.U_nom, b.U_out, b.diag, b.flags};
+        softmin_combine(o, recs, n, final_level, out_rec, write_record, s_hd, s_f);
+    };
+    // arrive on a ticket; true for the block that completes it (which resets it for the next step). The block's
+    // record writes reach thread 0 through the barrier and the device through its fence (the grid-barrier
+    // pattern: one fence per block, not one per thread -- 512 MEMBAR.SC.GPU cost microseconds on the tail)
+    auto last_arrival = [&](unsigned* ticket, unsigned count) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(ticket, 1u) == count - 1u;
+            if (s_last) {
+                *ticket = 0u;   // every arrival of this step is in (the kernel boundary orders the next step)
+                __threadfence();
             }
         }
-        const int t = tc >> 2, c = tc & 3;
-        if (write_record) {
-            b.record[(long long)bb * W + kRecHead + tc] = V;
-        } else {
-            const float Uv = b.U_nom[((long long)bb * p.T + t) * 4 + c];
-            b.U_out[((long long)bb * p.T + t) * 4 + c] = (ok && Sg > 0.f) ? Uv + V / Sg : Uv;
-        }
+        __syncthreads();
+        return s_last;
+    };
+    const int ngrp = softmin_groups(nblk);
+    if (ngrp == 0) {
+        if (!last_arrival(b.tickets + bb, (unsigned)(nblk * nz_t))) return;
+        SM_TRACE(6);
+        combine(b.blkrec + (long long)bb * nblk * W, nblk, true, nullptr);
+    } else {
+        const int g = blockIdx.x / kSoftminGroup, members = min(kSoftminGroup, nblk - g * kSoftminGroup);
+        float* grec = b.blkrec + (long long)p.n_ctrl * nblk * W + ((long long)bb * ngrp + g) * W;
+        if (!last_arrival(b.tickets + p.n_ctrl + (long long)bb * ngrp + g, (unsigned)(members * nz_t))) return;
+        combine(b.blkrec + ((long long)bb * nblk + (long long)g * kSoftminGroup) * W, members, false, grec);
+        if (!last_arrival(b.tickets + bb, (unsigned)ngrp)) return;
+        SM_TRACE(6);
+        combine(b.blkrec + (long long)p.n_ctrl * nblk * W + (long long)bb * ngrp * W, ngrp, true, nullptr);
     }
-    if (threadIdx.x == 0) {
-        if (write_record) {
-            float* out = b.record + (long long)bb * W;
-            out[0] = mg; out[1] = Sg; out[2] = S2g; out[3] = SJg;
-            out[4] = NJg; out[5] = out[6] = out[7] = 0.f;
-        } else {
-            float* d = b.diag + bb * 4;
-            d[0] = mg;
-            d[1] = Sg;
-            d[2] = S2g > 0.f ? Sg * Sg / S2g : 0.f;
-            d[3] = NJg > 0.f ? SJg / NJg : INFINITY;
-            b.flags[bb] = ok ? 0 : 1;
-        }
-        b.tickets[bb] = 0u;   // ready for the next step (kernel boundary orders it)
-    }
+    SM_TRACE(4);
 }
 
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s) {
@@ -574,6 +777,7 @@ void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaSt
 }
 
 int softmin_blocks(int K) { return (K + softmin_spb(K) - 1) / softmin_spb(K); }
+int softmin_group_count(int K) { return softmin_groups(softmin_blocks(K)); }
 
 // ------------------------------------------------------------------ shard combine (configs[3])
 // m = min_r m_r; S = sum_r S_r e^{-(m_r - m)/lambda}; V = sum_r V_r e^{...}; U* = U + V/S.

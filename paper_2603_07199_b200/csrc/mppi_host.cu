@@ -81,8 +81,8 @@ bool compute_layout(const mppi_config* c, Layout* L) {
     sz[B_TERMS] = 4 * n * T * K;
     sz[B_PART] = 4 * n * K;
     sz[B_J] = 4 * n * K;
-    sz[B_TICK] = 4 * n;
-    sz[B_BLKREC] = 4 * n * (size_t)softmin_blocks(c->K) * recw;
+    sz[B_TICK] = 4 * n * (1 + (size_t)softmin_group_count(c->K));
+    sz[B_BLKREC] = 4 * n * (size_t)(softmin_blocks(c->K) + softmin_group_count(c->K)) * recw;
     sz[B_REC] = 4 * n * recw;
     sz[B_GATH] = 4 * world * n * recw;
     sz[B_DIAG] = 16 * n;
@@ -379,7 +379,7 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         return cleanup(MPPI_ERR_CUDA, "work stream / events");
     // zero-init the small state (U, diag, flags, step) so debug reads are defined
     if (cudaMemsetAsync(base, 0, L.off[B_NOISE], ctx->stream) != cudaSuccess ||
-        cudaMemsetAsync(b.tickets, 0, 4 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(b.tickets, 0, 4 * (size_t)cfg->n_ctrl * (1 + softmin_group_count(cfg->K)), ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(b.diag, 0, 16 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(b.flags, 0, 4 * (size_t)cfg->n_ctrl, ctx->stream) != cudaSuccess)
         return cleanup(MPPI_ERR_CUDA, "memset");
@@ -846,6 +846,8 @@ int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries) {
     // H = 128 kernel (kernel_mlp_h128.cu) when MPPI_TRACE_H128=1, else the kernel_mlp_tc.cu timeline
     const char* h = getenv("MPPI_TRACE_H128");
     if (h && h[0] == '1') return mlp_h128_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
+    const char* sm = getenv("MPPI_TRACE_SOFTMIN");
+    if (sm && sm[0] == '1') return softmin_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
     return mlp_tc_trace_copy(reinterpret_cast<unsigned long long*>(host_out), max_entries);
 }
 

@@ -65,8 +65,8 @@ struct Buffers {
     float* terms;         // [n_ctrl*T*K] SDF-dependent stage cost
     float* partial;       // [n_ctrl*K] non-SDF cost sums
     float* J;             // [n_ctrl*K]
-    unsigned* tickets;    // [n_ctrl] blocks of k_softmin done this step (reset by the last block)
-    float* blkrec;        // [n_ctrl][softmin blocks][kRecHead + 4T] per-block records
+    unsigned* tickets;    // [n_ctrl] + [n_ctrl][groups] k_softmin arrivals this step (reset by the last block)
+    float* blkrec;        // [n_ctrl][softmin blocks][kRecHead + 4T] per-block records, then [n_ctrl][groups][...]
     float* record;        // [n_ctrl][kRecHead + 4T]  this rank's record
     float* gathered;      // [world][n_ctrl][kRecHead + 4T]
     float* weights;       // [n_ctrl][K] normalised softmin weights (debug, on demand)
@@ -81,6 +81,7 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
                      float* sdf_out, bool states_mode, cudaStream_t s);
 void launch_softmin(const Params& p, const Buffers& b, bool write_record, cudaStream_t s);
 int softmin_blocks(int K);
+int softmin_group_count(int K);   // group records / tickets of the two-level combine (0: one level)
 void launch_combine(const Params& p, const Buffers& b, const float* recs, int R, cudaStream_t s);
 void launch_fold(const Params& p, const Buffers& b, int ctrl_begin, int ctrl_count, cudaStream_t s);
 void launch_weights(const Params& p, const Buffers& b, cudaStream_t s);   // debug: normalised softmin weights
@@ -106,6 +107,7 @@ bool mlp_tc_pe_supported(int H, int n_gemm, int pe_bands);
 // H = 128 tcgen05 SDF-MLP with shared-memory A operands and layer 1 on the tensor cores (kernel_mlp_h128.cu)
 bool mlp_h128_supported(int n_gemm, int pe_bands);
 int mlp_h128_trace_copy(unsigned long long* host, int max_entries);   // debug builds (MPPI_TC_TRACE) only
+int softmin_trace_copy(unsigned long long* host, int max_entries);   // debug builds (MPPI_TC_TRACE) only
 size_t mlp_h128_image_bytes(int n_gemm, int pe_bands);   // hidden image (as mlp_tc_pack_weights) + layer-1 B
 void mlp_h128_pack_l1(int pe_bands, int act, const float* w1pos, uint8_t* out);
 // fuse: the rollout runs inside the kernel (CTBR model, guidance on, K % 64 == 0, states_mode): rows unused

@@ -309,3 +309,39 @@ def test_no_writes_outside_the_workspace(name, over):
             c.sdf_eval(synth.make_query_rows(131, seed=4)).cpu()
         assert c.guards_intact(), (name, mode)
         c.close()
+
+
+# ---------------------------------------------------------------- two-level softmin record combine
+
+@pytest.mark.parametrize("over", [{"n_ctrl": 1, "K": 8448, "T": 16},      # 33 blocks: groups 16+16+1, 2 T slices
+                                  {"n_ctrl": 2, "K": 9000, "T": 5},       # 36 blocks, ragged last block
+                                  {"n_ctrl": 1, "K": 70000, "T": 6}])     # 512-sample blocks: 137 -> 9 groups
+def test_two_level_softmin_combine(over):
+    """k_softmin from 33 sample blocks on combines in two levels (groups of 16, then the group records):
+    U* equals the float64 softmin of the step's own costs (Eq. 5) and the diagnostics
+    (J_min, S, ESS, mean J) are those of the same costs, over two steps (the tickets reset)."""
+    from scipy.special import softmax
+    cfg, Ws, bs, inp, ctrl = gh.setup("c1s", **over)
+    U = inp["U"]
+    for step in range(2):
+        if step:
+            noise = synth.make_noise(cfg, step=step)
+            ctrl.set_noise(noise)
+        else:
+            noise = inp["noise"]
+        ctrl.step(inp["x0"], inp["goal"], step)
+        Ug, _ = ctrl.get_controls()
+        J = ctrl.debug("costs").astype(np.float64)
+        d = ctrl.diagnostics().astype(np.float64)
+        for b in range(cfg.n_ctrl):
+            Ub = U[b] if step == 0 else np.concatenate([U[b][1:], U[b][-1:]], 0)
+            nb = np.asarray(noise)[:, b * cfg.K:(b + 1) * cfg.K]
+            prop = gh.softmin_property(cfg, Ub, nb, J[b])
+            assert np.abs(Ug[b] - prop).max() <= gh.ABS_U
+            w = softmax(-J[b] / cfg.lam)
+            assert d[b, 0] == J[b].min()
+            np.testing.assert_allclose(d[b, 1], np.exp(-(J[b] - J[b].min()) / cfg.lam).sum(), rtol=1e-4)
+            np.testing.assert_allclose(d[b, 2], 1.0 / (w ** 2).sum(), rtol=1e-3)
+            np.testing.assert_allclose(d[b, 3], J[b].mean(), rtol=1e-5)
+        U = Ug
+    ctrl.close()
