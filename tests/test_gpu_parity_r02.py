@@ -345,3 +345,44 @@ def test_two_level_softmin_combine(over):
             np.testing.assert_allclose(d[b, 3], J[b].mean(), rtol=1e-5)
         U = Ug
     ctrl.close()
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_sharded_record_mode_two_level(R):
+    """Record mode of k_softmin (configs[3] sharded: the rank's combined record instead of U*) through the
+    two-level combine (8448 samples per rank = 33 blocks): the gathered records combined on every rank equal
+    the unsharded context's update (the shard-combine identity, Eq. 5)."""
+    import torch
+    from paper_2603_07199_b200 import Controller
+    Kr = 8448
+    cfg = synth.get_config("c3s", K=R * Kr, T=4)
+    Ws, bs = synth.make_weights(cfg)
+    z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
+                          synth.make_goals(cfg), synth.make_nominal(cfg))
+    ctrls = []
+    for r in range(R):
+        c = Controller(cfg.replace(K=Kr), noise_mode="device", K_global=cfg.K, k_offset=r * Kr, world_size=R, rank=r)
+        c.set_sdf_weights(Ws, bs)
+        c.set_latent(z, Tq)
+        c.set_nominal(U)
+        c.step_local(x0, goal, 0)
+        ctrls.append(c)
+    recs = torch.from_numpy(np.stack([c.debug("record") for c in ctrls])).cuda()
+    outs = []
+    for c in ctrls:
+        c.step_finish(recs)
+        outs.append(c.get_controls()[0])
+        c.close()
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+    c1 = Controller(cfg, noise_mode="device", debug_outputs=True)
+    c1.set_sdf_weights(Ws, bs)
+    c1.set_latent(z, Tq)
+    c1.set_nominal(U)
+    c1.step(x0, goal, 0)
+    U1 = c1.get_controls()[0]
+    np.testing.assert_allclose(U1, outs[0], atol=1e-4)
+    J = c1.debug("costs").astype(np.float64)
+    prop = gh.softmin_property(cfg, U[0], c1.debug("noise").astype(np.float64), J[0])
+    assert np.abs(U1[0] - prop).max() <= gh.ABS_U
+    c1.close()
