@@ -81,6 +81,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_EPI_PIPE
 #define MPPI_EPI_PIPE -1   // -1: per configuration (see the epilogue); 0 / 1 force off / on
 #endif
+#ifndef MPPI_EPI_ALL
+#define MPPI_EPI_ALL -1   // -1: per configuration (H = 256 on); 0 / 1 force off / on
+#endif
 #ifndef MPPI_SPLITK
 #define MPPI_SPLITK 1
 #endif
@@ -759,13 +762,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     // H = 256: chunk k + 1's TMEM load is in flight while chunk k is computed (configs[2] -2%;
                     // H = 128 +2%: load, wait, compute)
-                    constexpr bool kPipe = MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0;
-                    uint32_t accb[kPipe ? 2 : 1][kCW];
+                    // kAll (H = 256): the whole D share of the warp (NCH x 16 columns) loaded at once, one wait, and
+                    // D released before any of it is computed, so the slot's next unit can start ~1 k cycles
+                    // earlier (the N-half-0 activations kept in registers are already stored at h = 1)
+                    constexpr bool kAll = MPPI_EPI_ALL < 0 ? CG == 2 : MPPI_EPI_ALL != 0;
+                    constexpr bool kPipe = !kAll && (MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0);
+                    uint32_t accb[kAll ? C::NCH : kPipe ? 2 : 1][kCW];
+                    if constexpr (kAll) {
+#pragma unroll
+                        for (int k = 0; k < C::NCH; ++k) tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), accb[k]);
+                        tmem_wait_ld_regs(accb[0]);
+#pragma unroll
+                        for (int k = 1; k < C::NCH; ++k) tmem_tie_regs(accb[k]);
+                    }
                     if constexpr (kPipe) tmem_ld16(tmem + lane_addr + d_col, accb[0]);
 #pragma unroll
                     for (int k = 0; k < C::NCH; ++k) {
-                        uint32_t(&acc)[kCW] = accb[kPipe ? (k & 1) : 0];
-                        if constexpr (kPipe) {
+                        uint32_t(&acc)[kCW] = accb[kAll ? k : kPipe ? (k & 1) : 0];
+                        if constexpr (kAll) {
+                        } else if constexpr (kPipe) {
                             tmem_wait_ld_regs(acc);
                             if (k + 1 < C::NCH)
                                 tmem_ld16(tmem + lane_addr + d_col + (uint32_t)((k + 1) * kCW), accb[(k + 1) & 1]);
@@ -773,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tmem_ld16(tmem + lane_addr + d_col + (uint32_t)(k * kCW), acc);
                             tmem_wait_ld_regs(acc);
                         }
-                        if (k == C::NCH - 1) {   // D of the slot may be overwritten now
+                        if (kAll ? k == 0 : k == C::NCH - 1) {   // D of the slot may be overwritten now
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) arrive_sched(BAR_DFREE + sl);
