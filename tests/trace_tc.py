@@ -34,8 +34,23 @@ def main():
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    step_mode = len(sys.argv) > 3 and sys.argv[3] == "step"   # a whole controller step (MPPI_FUSED=1: fused)
+    if step_mode:
+        from paper_2603_07199_b200 import Controller
+        cfg = synth.get_config(name)
+        sc = Controller(cfg, noise_mode="device")
+        sc.set_sdf_weights(Ws, bs)
+        sc.set_latent(synth.make_latents(cfg), synth.make_query_transforms(cfg))
+        sc.set_nominal(synth.make_nominal(cfg))
+        sc.step(synth.make_x0(cfg), synth.make_goals(cfg), 0)
+        sc.get_controls()
+        lib.mppi_debug_trace(buf.ctypes.data_as(C.c_void_p), cap)   # reset
+        print(f"fused rollout: {sc.fused_rollout()}")
     t0.record()
-    ctrl.sdf_eval(rows)
+    if step_mode:
+        sc.step(synth.make_x0(cfg), synth.make_goals(cfg), 1)
+    else:
+        ctrl.sdf_eval(rows)
     t1.record()
     torch.cuda.synchronize()
     print(f"{name}: {n} rows, {t0.elapsed_time(t1) * 1e3:.1f} us (with tracing)")
