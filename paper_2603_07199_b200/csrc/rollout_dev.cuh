@@ -64,75 +64,103 @@ __device__ __forceinline__ unsigned long long global_sample(const Params& p, int
 // Issue-bound at configs[3..4] (one thread per sample, T dependent steps): the state updates run as f32x2
 // pairs (FFMA2 / FADD2 on (px,py), (vx,vy), (qw,qx), (qy,qz); pz and vz scalar), the quaternion rates use the
 // half body rates, |v| is MUFU.SQRT (sqrt.approx, ~1 ulp) -- about 200 instructions per step instead of ~300.
-// xdot for the pair layout: a = (ax, ay), az, dq01 = (qw', qx'), dq23 = (qy', qz'); hw = half body rates
-__device__ __forceinline__ void dyn_ctbr2(float2 q01, float2 q23, float com2, float comg, float hwx, float hwy,
-                                         float hwz, float2& a, float& az, float2& dq01, float2& dq23) {
+// The CTBR step splits into an attitude half and a translational half: q evolves on its own (q' = 1/2 q (x) w,
+// w = the held body rates), and the translational dynamics read q only through the thrust direction terms of
+// the four RK4 stage attitudes. ctbr_att_step computes the clamped input, the attitude RK4 step (q renormalised)
+// and those stage terms; ctbr_trans_step the velocity / position RK4 step from them, the query rows and the
+// stage cost. ctbr_step runs both in one thread (k_rollout, the fused producers). Running the two halves on two
+// warps of a three-stage pipeline (noise / attitude / translation, 32 samples per block) was measured for the
+// small configurations and does not shorten the chain (configs[1] rollout 19.3 vs 19.5 us, configs[2] 25 vs
+// 27 us): within one thread the halves already overlap.
+struct CtbrStage {   // per step: thrust-direction terms of the 4 stage attitudes, u0, |u|^2
+    float bx[4], by[4], bz[4];
+    float u0, uu;
+};
+
+// (bx, by, bz) of one attitude: a = (c/m) 2 (bx, by), az = (c/m)(1 - 2 bz) - g
+__device__ __forceinline__ void ctbr_b3(float2 q01, float2 q23, float& bx, float& by, float& bz) {
     const float qw = q01.x, qx = q01.y, qy = q23.x, qz = q23.y;
-    a.x = com2 * fmaf(qx, qz, qw * qy);
-    a.y = com2 * fmaf(qy, qz, -qw * qx);
-    az = fmaf(-com2, fmaf(qx, qx, qy * qy), comg);       // (c/m)(1 - 2(qx^2 + qy^2)) - g
+    bx = fmaf(qx, qz, qw * qy);
+    by = fmaf(qy, qz, -qw * qx);
+    bz = fmaf(qx, qx, qy * qy);
+}
+// q' = 1/2 q (x) (0, w) with the half body rates hw
+__device__ __forceinline__ void ctbr_dq(float2 q01, float2 q23, float hwx, float hwy, float hwz, float2& dq01,
+                                       float2& dq23) {
+    const float qw = q01.x, qx = q01.y, qy = q23.x, qz = q23.y;
     dq01.x = fmaf(-qx, hwx, fmaf(-qy, hwy, -qz * hwz));
     dq01.y = fmaf(qw, hwx, fmaf(qy, hwz, -qz * hwy));
     dq23.x = fmaf(qw, hwy, fmaf(qz, hwx, -qx * hwz));
     dq23.y = fmaf(qw, hwz, fmaf(qx, hwy, -qy * hwx));
 }
 
-__device__ __forceinline__ void ctbr_step(const Params& p, float (&x)[10], float4 U, float4 n, const float (&R)[9],
-                                          const float (&tq)[3], const float (&gc)[3], float inv_mass, float4& row0,
-                                          float4& row1, float& part) {
-    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.f / 6.f), g = p.gravity;
+// attitude half: u = clamp(U*_t + sigma n) (R5), RK4 of q with u held (q renormalised), stage terms
+__device__ __forceinline__ void ctbr_att_step(const Params& p, float2& Q01, float2& Q23, float4 U, float4 n,
+                                              CtbrStage& st) {
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.f / 6.f);
     const float u0 = clampf(fmaf(p.sigma[0], n.x, U.x), p.u_lo[0], p.u_hi[0]);
     const float u1 = clampf(fmaf(p.sigma[1], n.y, U.y), p.u_lo[1], p.u_hi[1]);
     const float u2 = clampf(fmaf(p.sigma[2], n.z, U.z), p.u_lo[2], p.u_hi[2]);
     const float u3 = clampf(fmaf(p.sigma[3], n.w, U.w), p.u_lo[3], p.u_hi[3]);
-    const float com = u0 * inv_mass, com2 = 2.f * com, comg = com - g;
     const float hwx = 0.5f * u1, hwy = 0.5f * u2, hwz = 0.5f * u3;
-    const float2 P = make_float2(x[0], x[1]), V = make_float2(x[3], x[4]);
-    const float pz = x[2], vz = x[5];
-    const float2 Q01 = make_float2(x[6], x[7]), Q23 = make_float2(x[8], x[9]);
     const float2 H2 = make_float2(hdt, hdt), D2 = make_float2(dt, dt);
-    // stage 1 (k1: dP = V, dpz = vz)
-    float2 a1, dq01_1, dq23_1;
-    float az1;
-    dyn_ctbr2(Q01, Q23, com2, comg, hwx, hwy, hwz, a1, az1, dq01_1, dq23_1);
-    // stage 2 at x + hdt k1
-    const float2 V2 = __ffma2_rn(H2, a1, V);
-    const float vz2 = fmaf(hdt, az1, vz);
-    float2 a2, dq01_2, dq23_2;
-    float az2;
-    dyn_ctbr2(__ffma2_rn(H2, dq01_1, Q01), __ffma2_rn(H2, dq23_1, Q23), com2, comg, hwx, hwy, hwz, a2, az2, dq01_2,
-              dq23_2);
-    // stage 3 at x + hdt k2
-    const float2 V3 = __ffma2_rn(H2, a2, V);
-    const float vz3 = fmaf(hdt, az2, vz);
-    float2 a3, dq01_3, dq23_3;
-    float az3;
-    dyn_ctbr2(__ffma2_rn(H2, dq01_2, Q01), __ffma2_rn(H2, dq23_2, Q23), com2, comg, hwx, hwy, hwz, a3, az3, dq01_3,
-              dq23_3);
-    // stage 4 at x + dt k3
-    const float2 V4 = __ffma2_rn(D2, a3, V);
-    const float vz4 = fmaf(dt, az3, vz);
-    float2 a4, dq01_4, dq23_4;
-    float az4;
-    dyn_ctbr2(__ffma2_rn(D2, dq01_3, Q01), __ffma2_rn(D2, dq23_3, Q23), com2, comg, hwx, hwy, hwz, a4, az4, dq01_4,
-              dq23_4);
-    // x + dt/6 (k1 + 2 k2 + 2 k3 + k4); the position rates k_i are the stage velocities V, V2, V3, V4
+    float2 d01_1, d23_1, d01_2, d23_2, d01_3, d23_3, d01_4, d23_4;
+    ctbr_b3(Q01, Q23, st.bx[0], st.by[0], st.bz[0]);
+    ctbr_dq(Q01, Q23, hwx, hwy, hwz, d01_1, d23_1);
+    const float2 q01_2 = __ffma2_rn(H2, d01_1, Q01), q23_2 = __ffma2_rn(H2, d23_1, Q23);
+    ctbr_b3(q01_2, q23_2, st.bx[1], st.by[1], st.bz[1]);
+    ctbr_dq(q01_2, q23_2, hwx, hwy, hwz, d01_2, d23_2);
+    const float2 q01_3 = __ffma2_rn(H2, d01_2, Q01), q23_3 = __ffma2_rn(H2, d23_2, Q23);
+    ctbr_b3(q01_3, q23_3, st.bx[2], st.by[2], st.bz[2]);
+    ctbr_dq(q01_3, q23_3, hwx, hwy, hwz, d01_3, d23_3);
+    const float2 q01_4 = __ffma2_rn(D2, d01_3, Q01), q23_4 = __ffma2_rn(D2, d23_3, Q23);
+    ctbr_b3(q01_4, q23_4, st.bx[3], st.by[3], st.bz[3]);
+    ctbr_dq(q01_4, q23_4, hwx, hwy, hwz, d01_4, d23_4);
     const float2 T2 = make_float2(2.f, 2.f), S6 = make_float2(dt6, dt6);
-    const float2 sP = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(V2, V3), V), V4);
-    const float2 sV = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(a2, a3), a1), a4);
-    const float2 s01 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(dq01_2, dq01_3), dq01_1), dq01_4);
-    const float2 s23 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(dq23_2, dq23_3), dq23_1), dq23_4);
-    const float2 Pn = __ffma2_rn(S6, sP, P), Vn = __ffma2_rn(S6, sV, V);
-    const float pzn = fmaf(dt6, fmaf(2.f, vz2 + vz3, vz) + vz4, pz);
-    const float vzn = fmaf(dt6, fmaf(2.f, az2 + az3, az1) + az4, vz);
+    const float2 s01 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(d01_2, d01_3), d01_1), d01_4);
+    const float2 s23 = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(d23_2, d23_3), d23_1), d23_4);
     float2 q01 = __ffma2_rn(S6, s01, Q01), q23 = __ffma2_rn(S6, s23, Q23);
     const float qinv = rsqrtf(fmaf(q01.x, q01.x, fmaf(q01.y, q01.y, fmaf(q23.x, q23.x, q23.y * q23.y))));  // MUFU
     const float2 QI = make_float2(qinv, qinv);
-    q01 = __fmul2_rn(q01, QI);
-    q23 = __fmul2_rn(q23, QI);
-    x[0] = Pn.x; x[1] = Pn.y; x[2] = pzn; x[3] = Vn.x; x[4] = Vn.y; x[5] = vzn;
-    x[6] = q01.x; x[7] = q01.y; x[8] = q23.x; x[9] = q23.y;
-    // query-frame position and direction, scored at x_{t+1} (reading R7)
+    Q01 = __fmul2_rn(q01, QI);
+    Q23 = __fmul2_rn(q23, QI);
+    st.u0 = u0;
+    st.uu = fmaf(u0, u0, fmaf(u1, u1, fmaf(u2, u2, u3 * u3)));
+}
+
+// translational half: RK4 of (p, v) with the stage accelerations a_s = (c/m)(2 bx, 2 by, 1 - 2 bz) - g e_z,
+// then the query rows of x_{t+1} in the cached frame (p_c = R p + t_q, |v|) and (p_c + h v_c/|v|, 0)
+// (reading R7) and the non-SDF stage cost w_goal |p - g_c|^2 + w_u |u|^2
+__device__ __forceinline__ void ctbr_trans_step(const Params& p, float2& P, float& pz, float2& V, float& vz,
+                                                const CtbrStage& st, const float (&R)[9], const float (&tq)[3],
+                                                const float (&gc)[3], float inv_mass, float4& row0, float4& row1,
+                                                float& part) {
+    const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.f / 6.f), g = p.gravity;
+    const float com = st.u0 * inv_mass, com2 = 2.f * com, comg = com - g;
+    const float2 H2 = make_float2(hdt, hdt), D2 = make_float2(dt, dt);
+    float2 a[4];
+    float az[4];
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) {
+        a[s2] = make_float2(com2 * st.bx[s2], com2 * st.by[s2]);
+        az[s2] = fmaf(-com2, st.bz[s2], comg);
+    }
+    const float2 V2 = __ffma2_rn(H2, a[0], V);
+    const float vz2 = fmaf(hdt, az[0], vz);
+    const float2 V3 = __ffma2_rn(H2, a[1], V);
+    const float vz3 = fmaf(hdt, az[1], vz);
+    const float2 V4 = __ffma2_rn(D2, a[2], V);
+    const float vz4 = fmaf(dt, az[2], vz);
+    // x + dt/6 (k1 + 2 k2 + 2 k3 + k4); the position rates k_i are the stage velocities V, V2, V3, V4
+    const float2 T2 = make_float2(2.f, 2.f), S6 = make_float2(dt6, dt6);
+    const float2 sP = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(V2, V3), V), V4);
+    const float2 sV = __fadd2_rn(__ffma2_rn(T2, __fadd2_rn(a[1], a[2]), a[0]), a[3]);
+    P = __ffma2_rn(S6, sP, P);
+    const float vz0 = vz;
+    V = __ffma2_rn(S6, sV, V);
+    pz = fmaf(dt6, fmaf(2.f, vz2 + vz3, vz0) + vz4, pz);
+    vz = fmaf(dt6, fmaf(2.f, az[1] + az[2], az[0]) + az[3], vz0);
+    const float x[6] = {P.x, P.y, pz, V.x, V.y, vz};
     float pc[3], dv[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -144,7 +172,26 @@ __device__ __forceinline__ void ctbr_step(const Params& p, float (&x)[10], float
     row0 = make_float4(pc[0], pc[1], pc[2], nv);
     row1 = make_float4(fmaf(sc, dv[0], pc[0]), fmaf(sc, dv[1], pc[1]), fmaf(sc, dv[2], pc[2]), 0.f);
     const float dx = x[0] - gc[0], dy = x[1] - gc[1], dz = x[2] - gc[2];
-    part += p.w_goal * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) + p.w_u * fmaf(u0, u0, fmaf(u1, u1, fmaf(u2, u2, u3 * u3)));
+    part += p.w_goal * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) + p.w_u * st.uu;
+}
+
+// One CTBR rollout step of one sample in one thread (readings R4, R5, R7, R11, R12): the
+// attitude half then the translational half. Shared by k_rollout and the fused rollout producers of the SDF-MLP
+// kernels, so all produce the same rows.
+// Issue-bound at configs[3..4]: the state updates run as f32x2 pairs (FFMA2 / FADD2 on (px,py), (vx,vy),
+// (qw,qx), (qy,qz); pz and vz scalar), the quaternion rates use the half body rates, |v| is MUFU.SQRT
+// (sqrt.approx, ~1 ulp).
+__device__ __forceinline__ void ctbr_step(const Params& p, float (&x)[10], float4 U, float4 n, const float (&R)[9],
+                                          const float (&tq)[3], const float (&gc)[3], float inv_mass, float4& row0,
+                                          float4& row1, float& part) {
+    float2 P = make_float2(x[0], x[1]), V = make_float2(x[3], x[4]);
+    float pz = x[2], vz = x[5];
+    float2 Q01 = make_float2(x[6], x[7]), Q23 = make_float2(x[8], x[9]);
+    CtbrStage st;
+    ctbr_att_step(p, Q01, Q23, U, n, st);
+    ctbr_trans_step(p, P, pz, V, vz, st, R, tq, gc, inv_mass, row0, row1, part);
+    x[0] = P.x; x[1] = P.y; x[2] = pz; x[3] = V.x; x[4] = V.y; x[5] = vz;
+    x[6] = Q01.x; x[7] = Q01.y; x[8] = Q23.x; x[9] = Q23.y;
 }
 
 }  // namespace mppi
