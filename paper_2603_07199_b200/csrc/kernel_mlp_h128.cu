@@ -437,6 +437,9 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
         auto store_a = [&](int j0, const uint32_t* packed) {
             const int kc = j0 / 64, c0 = (j0 % 64) / 8;
             const uint32_t rb = aA + (uint32_t)(kc * (kRows * 128) + r * 128);
+#ifdef H128_NO_STORE_A
+            if (p.K != -12345) return;   // timing probe only (wrong results): the epilogue's A stores skipped
+#endif
 #pragma unroll
             for (int c = 0; c < 2; ++c)
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (uint32_t)((((c0 + c) ^ (r & 7))) * 16)),
