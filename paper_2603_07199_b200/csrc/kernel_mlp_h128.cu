@@ -62,6 +62,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_A1_HELPER
 #define H128_A1_HELPER 0   // 1: warps 2-3 build the layer-1 operands (measured +3% at configs[4]: off)
 #endif
+#ifndef H128_STAG
+#define H128_STAG 0   // > 0: staggered issue order (slot s starts H128_STAG * s visits late)
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -359,54 +362,80 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
             // slower at configs[4].)
             constexpr uint32_t idesc = idesc_bf16(128, 128);
             mbar_wait(bar(BAR_W), 0);
+            // unit u of slot sl's n-th tile (local tile i0 + sl, i0 = n NS): wait for its operands, issue, commit
+            auto issue_unit = [&](int sl, int u, uint32_t n, long long i0) {
+                const uint32_t d_t = tmem + (uint32_t)(sl * 128);
+                const uint32_t a0 = sbase + (uint32_t)(C::OFF_A + sl * C::A_BYTES);
+                if (lane == 0) H_TRACE(0, 0, u, i0 + sl);
+                if (u == 0) {
+                    if (n > 0) issuer_wait(bar(BAR_DFREE + sl), (n - 1) & 1u);
+                    issuer_wait(bar(BAR_SA1 + sl), n & 1u);
+                } else {
+                    issuer_wait(bar(BAR_AREADY + sl), (n * (uint32_t)G + (uint32_t)(u - 1)) & 1u);
+                }
+                tc_fence_after();
+                if (lane == 0) H_TRACE(0, 1, u, i0 + sl);
+                if (elect_one()) {
+                    if (u == 0) {
+                        const uint32_t b0 = sbase + (uint32_t)C::OFF_B1;
+#pragma unroll
+                        for (int j = 0; j < C::K1 / 16; ++j)
+                            tc_mma_ss<1>(d_t, smem_desc_noswz(a0 + (uint32_t)(j * 256), 128, C::K1C * 128),
+                                         smem_desc_noswz(b0 + (uint32_t)(j * 256), 128, C::K1C * 128), idesc,
+                                         j > 0 ? 1u : 0u);
+                    } else {
+                        const int l = u - 1;
+                        // D = bias (ones x [b_hi, b_lo]), then D += A W_l^T over K = 128
+#ifndef H128_NO_BIAS_MMA
+                        tc_mma_ss<1>(d_t, smem_desc_noswz(sbase + (uint32_t)C::OFF_ONES, 128, 0),
+                                     smem_desc_noswz(sbase + (uint32_t)(C::OFF_BIAS + l * C::BIAS_UNIT), 128, 256),
+                                     idesc, 0u);
+#endif
+                        const uint32_t w0 = sbase + (uint32_t)(l * H * H * 2);
+#pragma unroll
+                        for (int j = 0; j < H / 16; ++j) {
+                            const uint32_t off = (uint32_t)((j / 4) * (kRows * 128) + (j % 4) * 32);
+                            tc_mma_ss<1>(d_t, smem_desc_sw128(a0 + off), smem_desc_sw128(w0 + off), idesc, 1u);
+                        }
+                    }
+                    tc_commit<1>(bar(BAR_MMA + sl));
+                    // a second commit of the last GEMM for the layer-1 builder (its own barrier: waiting on
+                    // BAR_MMA's parity could alias a phase two commits back)
+                    if (C::HELPER && u == G) tc_commit<1>(bar(BAR_AFREE + sl));
+                }
+                __syncwarp();
+                if (lane == 0) H_TRACE(0, 2, u, i0 + sl);
+            };
+#if H128_STAG > 0
+            // staggered order: the issuer visits the slots round-robin and each visit issues the slot's next unit;
+            // slot s joins H128_STAG * s visits late, so the slots' epilogue phases (layer 1, GEMM, output) do not
+            // all coincide. Per-slot unit counters, compile-time indexed (the visit loop is unrolled over the slots)
+            uint32_t cnt[NS], lim[NS];
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2) {
+                cnt[s2] = 0u;
+                lim[s2] = (uint32_t)((n_my > s2 ? (n_my - s2 + NS - 1) / NS : 0) * (G + 1));
+            }
+            for (uint32_t round = 0;; ++round) {
+                bool any = false;
+#pragma unroll
+                for (int sl = 0; sl < NS; ++sl) {
+                    if (cnt[sl] < lim[sl]) any = true;
+                    if (round < (uint32_t)(H128_STAG * sl) || cnt[sl] >= lim[sl]) continue;
+                    const uint32_t n = cnt[sl] / (uint32_t)(G + 1);
+                    issue_unit(sl, (int)(cnt[sl] - n * (uint32_t)(G + 1)), n, (long long)n * NS);
+                    ++cnt[sl];
+                }
+                if (!any) break;
+            }
+#else
             for (long long i0 = 0; i0 < n_my; i0 += NS) {
                 const uint32_t n = (uint32_t)(i0 / NS);
                 const int ns = (int)min((long long)NS, n_my - i0);
                 for (int u = 0; u <= G; ++u)
-                    for (int sl = 0; sl < ns; ++sl) {
-                        const uint32_t d_t = tmem + (uint32_t)(sl * 128);
-                        const uint32_t a0 = sbase + (uint32_t)(C::OFF_A + sl * C::A_BYTES);
-                        if (lane == 0) H_TRACE(0, 0, u, i0 + sl);
-                        if (u == 0) {
-                            if (n > 0) issuer_wait(bar(BAR_DFREE + sl), (n - 1) & 1u);
-                            issuer_wait(bar(BAR_SA1 + sl), n & 1u);
-                        } else {
-                            issuer_wait(bar(BAR_AREADY + sl), (n * (uint32_t)G + (uint32_t)(u - 1)) & 1u);
-                        }
-                        tc_fence_after();
-                        if (lane == 0) H_TRACE(0, 1, u, i0 + sl);
-                        if (elect_one()) {
-                            if (u == 0) {
-                                const uint32_t b0 = sbase + (uint32_t)C::OFF_B1;
-#pragma unroll
-                                for (int j = 0; j < C::K1 / 16; ++j)
-                                    tc_mma_ss<1>(d_t, smem_desc_noswz(a0 + (uint32_t)(j * 256), 128, C::K1C * 128),
-                                                 smem_desc_noswz(b0 + (uint32_t)(j * 256), 128, C::K1C * 128), idesc,
-                                                 j > 0 ? 1u : 0u);
-                            } else {
-                                const int l = u - 1;
-                                // D = bias (ones x [b_hi, b_lo]), then D += A W_l^T over K = 128
-#ifndef H128_NO_BIAS_MMA
-                                tc_mma_ss<1>(d_t, smem_desc_noswz(sbase + (uint32_t)C::OFF_ONES, 128, 0),
-                                             smem_desc_noswz(sbase + (uint32_t)(C::OFF_BIAS + l * C::BIAS_UNIT), 128, 256),
-                                             idesc, 0u);
-#endif
-                                const uint32_t w0 = sbase + (uint32_t)(l * H * H * 2);
-#pragma unroll
-                                for (int j = 0; j < H / 16; ++j) {
-                                    const uint32_t off = (uint32_t)((j / 4) * (kRows * 128) + (j % 4) * 32);
-                                    tc_mma_ss<1>(d_t, smem_desc_sw128(a0 + off), smem_desc_sw128(w0 + off), idesc, 1u);
-                                }
-                            }
-                            tc_commit<1>(bar(BAR_MMA + sl));
-                            // a second commit of the last GEMM for the layer-1 builder (its own barrier: waiting on
-                            // BAR_MMA's parity could alias a phase two commits back)
-                            if (C::HELPER && u == G) tc_commit<1>(bar(BAR_AFREE + sl));
-                        }
-                        __syncwarp();
-                        if (lane == 0) H_TRACE(0, 2, u, i0 + sl);
-                    }
+                    for (int sl = 0; sl < ns; ++sl) issue_unit(sl, u, n, i0);
             }
+#endif
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REGS_EPI));
