@@ -55,14 +55,20 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, extra
         src, obj = src_obj
         key = hashlib.sha256(open(src, "rb").read() + hdr_hash.encode()).hexdigest()[:24]
         cached = os.path.join(cache, f"{os.path.basename(src)}.{key}.o")
-        if os.path.exists(cached) and not verbose:
-            shutil.copyfile(cached, obj)
-            return subprocess.CompletedProcess([], 0, "", "")
+        try:
+            if os.path.exists(cached) and not verbose:
+                shutil.copyfile(cached, obj)
+                return subprocess.CompletedProcess([], 0, "", "")
+        except OSError:
+            pass
         r = subprocess.run([nvcc, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
         if r.returncode == 0:
-            os.makedirs(cache, exist_ok=True)
-            shutil.copyfile(obj, cached + f".{os.getpid()}")
-            os.replace(cached + f".{os.getpid()}", cached)
+            try:   # the cache is an optimisation only
+                os.makedirs(cache, exist_ok=True)
+                shutil.copyfile(obj, cached + f".{os.getpid()}")
+                os.replace(cached + f".{os.getpid()}", cached)
+            except OSError:
+                pass
         return r
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=len(objs)) as ex:
