@@ -57,7 +57,10 @@ void launch_noise_shift(const Params& p, const Buffers& b, bool gen, cudaStream_
 
 // ------------------------------------------------------------------ K1: rollout
 // K1 rollout: one thread per (controller, sample); state in registers; time-major noise read as float4.
-constexpr int kRolloutBlock = 64;   // small blocks: K/64 blocks spread the latency-bound rollout over all SMs
+#ifndef MPPI_RO_BLOCK
+#define MPPI_RO_BLOCK 64
+#endif
+constexpr int kRolloutBlock = MPPI_RO_BLOCK;   // small blocks: K/64 blocks spread the latency-bound rollout over all SMs
 
 // Device-noise producer warps of a rollout block (DEV): they generate the Philox normals of step t+1
 // (and store them for k_softmin) while the consumer warps integrate step t, handing them over through a
@@ -389,7 +392,10 @@ void launch_mlp_simt(const Params& p, const Buffers& b, const float4* rows, long
 // write_record: the combined record is this rank's record for the cross-rank combine (configs[3]).
 constexpr int kSoftminThreads = 512;   // 512/SPB threads per sample in phase 1, 16 warps over t in phase 2
 // samples per block: 256, or 512 from K = 65536 on (configs[3]: 256 blocks, one wave at 2 blocks per SM)
-__host__ __device__ constexpr int softmin_spb(int K) { return K >= 65536 ? 512 : 256; }
+#ifndef MPPI_SOFTMIN_K512
+#define MPPI_SOFTMIN_K512 65536
+#endif
+__host__ __device__ constexpr int softmin_spb(int K) { return K >= MPPI_SOFTMIN_K512 ? 512 : 256; }
 // two-level record combine from 33 sample blocks on: groups of kSoftminGroup (0 = one level)
 constexpr int kSoftminGroup = 16;
 __host__ __device__ constexpr int softmin_groups(int nblk) { return nblk > 32 ? (nblk + kSoftminGroup - 1) / kSoftminGroup : 0; }
