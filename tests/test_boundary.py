@@ -82,3 +82,14 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src).lower().replace("oracle/", ""), f
+
+
+def test_largest_problem_boundary(lib):
+    """The index space of a context: query rows n_ctrl K T (2 with guidance) up to 2^30 (32-bit tile / row
+    arithmetic in the kernels) -- the largest accepted size is sized, one step above it is rejected."""
+    from paper_2603_07199_b200._lib import make_config
+    top = synth.get_config("c1").replace(K=1 << 22, T=127)          # 1.065e9 rows
+    nb = lib.mppi_workspace_bytes(C.byref(make_config(top)))
+    assert nb > 0 and nb < 64 * 2 ** 30                              # ~33 GB of the 180 GB
+    assert lib.mppi_workspace_bytes(C.byref(make_config(top.replace(T=128)))) == 0   # 2^30 + ... rows
+    assert lib.mppi_workspace_bytes(C.byref(make_config(top.replace(T=128, w_guide=0.0)))) > 0

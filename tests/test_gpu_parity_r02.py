@@ -414,3 +414,34 @@ def test_long_horizon_step_parity(name, over):
         prop = gh.softmin_property(cfg, Ub, np.asarray(noise2)[:, b * cfg.K:(b + 1) * cfg.K], J[b])
         assert np.abs(Ug[b] - prop).max() <= gh.ABS_U
     ctrl.close()
+
+
+# ---------------------------------------------------------------- the largest accepted problem
+
+def test_largest_problem_sampled_costs():
+    """One context at the top of the index space (configs[1]'s MLP, K = 2^22 samples, T = 127: 1.065e9 query
+    rows, 32-bit row arithmetic near its limit): the costs of sampled rollouts at the high end of the sample
+    range -- their rows run up to index ~2^30 -- against the oracle recomputed one by one (global Philox
+    counters), and a finite update inside the input bounds."""
+    from paper_2603_07199_b200 import Controller
+    cfg = synth.get_config("c1").replace(K=1 << 22, T=127, dt=0.008)
+    Ws, bs = synth.make_weights(cfg)
+    z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
+                          synth.make_goals(cfg), synth.make_nominal(cfg))
+    ctrl = Controller(cfg, noise_mode="device")
+    ctrl.set_sdf_weights(Ws, bs)
+    ctrl.set_latent(z, Tq)
+    ctrl.set_nominal(U)
+    ctrl.step(x0, goal, 3)
+    Ug, _ = ctrl.get_controls()
+    J = ctrl.debug("costs").astype(np.float64)
+    oc = oracle.make_cfg(cfg)
+    for k in [cfg.K - 1, cfg.K - 2, cfg.K - 33, cfg.K // 2 + 5, 0]:
+        nz = oracle.noise(cfg.seed, 3, int(k), 1, cfg.T)[:, 0]
+        r = oracle.rollout(oc, Ws, bs, z[0], Tq[0], x0[0], goal[0], U[0], nz)
+        ref = {"queries": r["queries"][None, None], "sdf": r["sdf"][None, None], "stage": r["stage"][None, None]}
+        tol = gh.cost_tol(cfg, ref, gh.ABS_SDF_BF16)[0, 0]
+        assert abs(J[0, k] - r["J"]) <= tol, (k, J[0, k], r["J"], tol)
+    assert np.isfinite(Ug).all()
+    assert (Ug >= np.array(cfg.u_lo) - 1e-4).all() and (Ug <= np.array(cfg.u_hi) + 1e-4).all()
+    ctrl.close()
