@@ -418,13 +418,14 @@ def test_long_horizon_step_parity(name, over):
 
 # ---------------------------------------------------------------- the largest accepted problem
 
-def test_largest_problem_sampled_costs():
-    """One context at the top of the index space (configs[1]'s MLP, K = 2^22 samples, T = 127: 1.065e9 query
+@pytest.mark.parametrize("base", ["c1", "c2"])   # H = 128 (k_mlp_h128) and H = 256 (k_mlp_tc CTA pairs)
+def test_largest_problem_sampled_costs(base):
+    """One context at the top of the index space (configs[1]'s / [2]'s MLP, K = 2^22 samples, T = 127: 1.065e9 query
     rows, 32-bit row arithmetic near its limit): the costs of sampled rollouts at the high end of the sample
     range -- their rows run up to index ~2^30 -- against the oracle recomputed one by one (global Philox
     counters), and a finite update inside the input bounds."""
     from paper_2603_07199_b200 import Controller
-    cfg = synth.get_config("c1").replace(K=1 << 22, T=127, dt=0.008)
+    cfg = synth.get_config(base).replace(K=1 << 22, T=127, dt=0.008)
     Ws, bs = synth.make_weights(cfg)
     z, Tq, x0, goal, U = (synth.make_latents(cfg), synth.make_query_transforms(cfg), synth.make_x0(cfg),
                           synth.make_goals(cfg), synth.make_nominal(cfg))
