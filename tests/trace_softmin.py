@@ -40,7 +40,7 @@ def main():
     if last.any():   # stale stamps of earlier steps' last blocks may remain: the latest is this step's
         i = int(np.argmax(np.where(last, r[:, 4], 0)))
         print(f"  last block {i}: phase 2 done {st[i, 3]:.2f}, combine done {st[i, 4]:.2f} (tail {st[i, 4] - st[i, 3]:.2f})")
-        print(f"    final ticket won {(r[i, 6] - t0) / 1e3:.2f} (the group level before it), U* written {st[i, 4]:.2f}")
+        print(f"    final ticket won {(r[i, 6] - t0) / 1e3:.2f} (two-level: after this SM's group combine), U* written {st[i, 4]:.2f}")
     sms = r[:, 5]
     print(f"  distinct SMs {len(set(sms.tolist()))}; blocks per SM max {np.bincount(sms).max()}")
     order = np.argsort(st[:, 0])
