@@ -62,6 +62,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_A1_HELPER
 #define H128_A1_HELPER 0   // 1: warps 2-3 build the layer-1 operands (measured +3% at configs[4]: off)
 #endif
+#ifndef H128_DYN
+#define H128_DYN 0   // 1: ready-first issue order over the slots (non-blocking probes)
+#endif
 #ifndef H128_STAG
 #define H128_STAG 0   // > 0: staggered issue order (slot s starts H128_STAG * s visits late)
 #endif
@@ -406,7 +409,51 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                 __syncwarp();
                 if (lane == 0) H_TRACE(0, 2, u, i0 + sl);
             };
-#if H128_STAG > 0
+#if H128_DYN
+            // ready-first order: each round the issuer takes, among the slots whose next unit's operands are ready
+            // (non-blocking mbarrier probes), the one earliest in the round-robin order (key = units issued x NS +
+            // slot), so a slot still in its epilogue never holds back a ready one
+            uint32_t cnt[NS], lim[NS];
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2) {
+                cnt[s2] = 0u;
+                lim[s2] = (uint32_t)((n_my > s2 ? (n_my - s2 + NS - 1) / NS : 0) * (G + 1));
+            }
+            uint32_t spins = 0;
+            for (;;) {
+                int pick = -1;
+                uint32_t best = 0xFFFFFFFFu;
+                bool pending = false;
+#pragma unroll
+                for (int s2 = 0; s2 < NS; ++s2) {
+                    if (cnt[s2] >= lim[s2]) continue;
+                    pending = true;
+                    const uint32_t key = cnt[s2] * (uint32_t)NS + (uint32_t)s2;
+                    if (key >= best) continue;
+                    const uint32_t n = cnt[s2] / (uint32_t)(G + 1);
+                    const uint32_t u = cnt[s2] - n * (uint32_t)(G + 1);
+                    const bool rdy = u == 0 ? ((n == 0 || mbar_test(bar(BAR_DFREE + s2), (n - 1) & 1u)) &&
+                                               mbar_test(bar(BAR_SA1 + s2), n & 1u))
+                                            : mbar_test(bar(BAR_AREADY + s2), (n * (uint32_t)G + u - 1) & 1u);
+                    if (rdy) {
+                        best = key;
+                        pick = s2;
+                    }
+                }
+                if (!pending) break;
+                if (pick < 0) {
+                    if (++spins > (1u << 28)) __trap();
+                    continue;
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < NS; ++s2)
+                    if (s2 == pick) {
+                        const uint32_t n = cnt[s2] / (uint32_t)(G + 1);
+                        issue_unit(s2, (int)(cnt[s2] - n * (uint32_t)(G + 1)), n, (long long)n * NS);
+                        ++cnt[s2];
+                    }
+            }
+#elif H128_STAG > 0
             // staggered order: the issuer visits the slots round-robin and each visit issues the slot's next unit;
             // slot s joins H128_STAG * s visits late, so the slots' epilogue phases (layer 1, GEMM, output) do not
             // all coincide. Per-slot unit counters, compile-time indexed (the visit loop is unrolled over the slots)
