@@ -173,8 +173,15 @@ struct PEWeights {
     float2 w[NPAIR * NPE];
 };
 struct NoPEWeights {};
+// MPPI_L1_PARAM=1: without PE too, the H = 256 kernel takes its 3 x 256 position weights from the launch parameters
+// instead of two shared-memory loads per neuron pair (which share the MIO queue with the MUFU work). FFMA2 has no
+// constant-bank operand, so each weight pair becomes an LDC.64: measured +13% (configs[2]) / +8% (configs[3]); off.
+#ifndef MPPI_L1_PARAM
+#define MPPI_L1_PARAM 0
+#endif
 template <int H, int G, int PEB>
-using PEArg = typename std::conditional<(PEB > 0 && H == 256), PEWeights<H / 2, 3 + 6 * PEB>, NoPEWeights>::type;
+using PEArg = typename std::conditional<(H == 256 && (PEB > 0 || MPPI_L1_PARAM)), PEWeights<H / 2, 3 + 6 * PEB>,
+                                        NoPEWeights>::type;
 
 // FUSE (H = 256 CTA pairs, configs[3]-sized problems): the rows are not read from HBM. Warps 2-3 of each CTA
 // roll out its 64 samples of the pair's 128-sample block over the whole horizon with the device code of
@@ -619,10 +626,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int i2 = 0; i2 < kCW; i2 += 2) {
                             const int jp = (j0 + i2) / 2;   // neuron pair (j0+i2, j0+i2+1)
-                            const float4 wa = s_w1xy[jp];
-                            const float2 x = ffma2(make_float2(wa.x, wa.y), qx2,
-                                                   ffma2(make_float2(wa.z, wa.w), qy2,
-                                                         ffma2(s_w1z[jp], qz2, *reinterpret_cast<const float2*>(b1g + j0 + i2))));
+                            float2 wx, wy, wz;
+                            if constexpr (sizeof(pew) > 1) {   // weights in the launch parameters (H = 256)
+                                wx = pew.w[jp * 3]; wy = pew.w[jp * 3 + 1]; wz = pew.w[jp * 3 + 2];
+                            } else {
+                                const float4 wa = s_w1xy[jp];
+                                wx = make_float2(wa.x, wa.y); wy = make_float2(wa.z, wa.w); wz = s_w1z[jp];
+                            }
+                            const float2 x = ffma2(wx, qx2, ffma2(wy, qy2, ffma2(wz, qz2, *reinterpret_cast<const float2*>(b1g + j0 + i2))));
                             packed[i2 / 2] = act_pack<ACT>(x.x, x.y);
                         }
                     } else {   // rare: the tile crosses a controller boundary
@@ -950,7 +961,7 @@ cudaError_t launch_t(const Params& p, const Buffers& b, const float4* rows, long
     const long long groups = tiles < max_groups[dev] ? tiles : max_groups[dev];
     cfg.gridDim = dim3((unsigned)(groups * C::CG));
     PEArg<H, G, PEB> pew{};
-    if constexpr (PEB > 0 && H == 256) {
+    if constexpr (sizeof(PEArg<H, G, PEB>) > 1) {
         if (!b.w1pe2_host) return cudaErrorInvalidValue;
         std::memcpy(pew.w, b.w1pe2_host, sizeof(pew.w));
     }
