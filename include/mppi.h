@@ -225,8 +225,10 @@ int32_t mppi_kernels_per_step(const mppi_ctx* ctx);
  * the query rows then never reach HBM and MPPI_DBG_QUERIES returns MPPI_ERR_NOT_READY. */
 int32_t mppi_fused_rollout(const mppi_ctx* ctx);
 
-/* Debug builds only (compiled with -DMPPI_TC_TRACE): copy up to max_entries clock64 timeline records
- * of the SDF-MLP kernel's first CTAs to host_out and reset the log; returns the count (0 in release). */
+/* Debug builds only (compiled with -DMPPI_TC_TRACE): copy up to max_entries timeline records to host_out and
+ * return the count (0 in release builds). Which log: env MPPI_TRACE_H128=1 the H = 128 SDF-MLP kernel
+ * (clock64 records of its first CTAs), MPPI_TRACE_SOFTMIN=1 k_softmin ([1024 blocks][10] %globaltimer stamps of
+ * controller 0), else the H = 256 SDF-MLP kernel. Test tooling (tests/trace_*.py); not part of the method. */
 int32_t mppi_debug_trace(uint64_t* host_out, int32_t max_entries);
 
 const char* mppi_last_error(void);
