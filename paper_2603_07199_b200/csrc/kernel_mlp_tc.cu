@@ -93,6 +93,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_L1_MMA
 #define MPPI_L1_MMA 0   // H = 256: layer 1 as a K = 32 MMA on exact bf16 splits (see Cfg::L1M; A/B: +28% at configs[2])
 #endif
+#ifndef MPPI_PE_MMA
+#define MPPI_PE_MMA 1   // H = 256 with PE: the 27 position features as a K = 96 exact-split MMA (Cfg::L1PE)
+#endif
 constexpr int kTileRows = 128;
 
 // ------------------------------------------------------------------ configuration
@@ -116,8 +119,17 @@ struct Cfg {
     // H = 256: layer 1 runs on the tensor cores like the hidden layers (two N-half units of K = 32: the exact
     // three-part bf16 splits of p_c and W1p, six cross products per coordinate, as kernel_mlp_h128.cu), so its
     // epilogue is a GEMM epilogue (D + b1', act, pack) instead of a CUDA-core 3-wide dot per neuron pair
-    static constexpr bool L1M = CG == 2 && PEB == 0 && MPPI_L1_MMA;
-    static constexpr int NROWBUF = L1M ? NSLOT : 2 * NSLOT;  // query-row buffers (L1M: |v| kept in registers)
+    static constexpr bool L1M = CG == 2 && (PEB == 0 ? MPPI_L1_MMA : MPPI_PE_MMA);
+    // L1PE (H = 256 with PE, reading E2): layer 1 is one MMA unit per N-half over K1 = 96 operand columns -- raw p
+    // in the six-product split (18), each of the 24 sin/cos features as f_h w_h, f_h w_l, f_l w_h (72), 6 zero.
+    // Its B operand (24 KB per CTA) takes the shared memory of the bias MMA images and the row buffers: the
+    // hidden biases are added in the epilogue (FFMA2) and each thread loads its query row itself, one tile ahead.
+    static constexpr bool L1PE = L1M && PEB > 0;
+    static constexpr int K1_USED = 18 + 18 * PEB;                     // layer-1 operand columns in use
+    static constexpr int K1 = (K1_USED + 15) / 16 * 16;              // 32, or 96 with 4 PE bands
+    static constexpr int K1S = K1 / 16;                              // K = 16 MMA steps of layer 1
+    static constexpr bool BIAS_MMA = !L1PE;                          // hidden biases by a ones x bias MMA
+    static constexpr int NROWBUF = L1PE ? 0 : L1M ? NSLOT : 2 * NSLOT;   // query-row buffers (L1M: |v| in registers)
     static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
     static constexpr int MMA_M = 128 * CG;
@@ -135,16 +147,17 @@ struct Cfg {
     // "ones" tile [128 rows][1, 1, 0 x 14], B = [b_hi, b_lo, 0 x 14] per output row (bf16 split of the
     // kP-scaled fp32 bias), both no-swizzle K-major -- so the epilogue adds nothing
     static constexpr int BIAS_UNIT = RB * 32;                        // RB rows x 16 bf16
-    static constexpr int BIAS_BYTES = G * NH * BIAS_UNIT;
-    static constexpr int IMG_BYTES = W_BYTES + BIAS_BYTES;           // weight image per CTA (rank)
+    static constexpr int IMG_BYTES = W_BYTES + G * NH * BIAS_UNIT;   // weight image per CTA (rank), global stride
+    static constexpr int BIAS_BYTES = BIAS_MMA ? G * NH * BIAS_UNIT : 0;   // bias images in shared memory
     static constexpr int OFF_BIAS = W_BYTES;
     static constexpr int OFF_ONES = OFF_BIAS + BIAS_BYTES;           // [128 rows][16] bf16 ones tile
-    static constexpr int OFF_WO = OFF_ONES + kTileRows * 32;         // [H] output weights
+    static constexpr int OFF_HB = OFF_ONES + (BIAS_MMA ? kTileRows * 32 : 0);   // !BIAS_MMA: [G][H] kP b (fp32)
+    static constexpr int OFF_WO = OFF_HB + (BIAS_MMA ? 0 : 4 * G * H);         // [H] output weights
     static constexpr int OFF_W1XY = OFF_WO + 4 * H;                  // [H/2] (w0x, w1x, w0y, w1y) layer-1 positions, scaled
     static constexpr int OFF_W1Z = OFF_W1XY + (L1M ? 0 : 8 * H);     // [H/2] (w0z, w1z)
     static constexpr int BL1_TILE = RB * 32;                         // L1M: per (unit, K step) RB rows x 16 bf16
     static constexpr int OFF_BL1 = OFF_W1Z + (L1M ? 0 : 4 * H);      // L1M: [NH][2 K steps] no-swizzle K-major
-    static constexpr int OFF_B1 = OFF_BL1 + (L1M ? NH * 2 * BL1_TILE : 0);   // [NSLOT groups][H] folded bias b1', scaled
+    static constexpr int OFF_B1 = OFF_BL1 + (L1M ? NH * K1S * BL1_TILE : 0);   // [NSLOT groups][H] folded bias b1', scaled
     // PEB > 0: [H/2][NPE] float2 PE weights (scaled) in shared memory at H = 128; at H = 256 the resident hidden
     // weights leave no room, so layer 1 reads the same pair-major image from global memory (L1-cached,
     // warp-uniform addresses)
@@ -180,7 +193,7 @@ struct NoPEWeights {};
 #define MPPI_L1_PARAM 0
 #endif
 template <int H, int G, int PEB>
-using PEArg = typename std::conditional<(H == 256 && (PEB > 0 || MPPI_L1_PARAM)), PEWeights<H / 2, 3 + 6 * PEB>,
+using PEArg = typename std::conditional<(H == 256 && ((PEB > 0 && !MPPI_PE_MMA) || MPPI_L1_PARAM)), PEWeights<H / 2, 3 + 6 * PEB>,
                                         NoPEWeights>::type;
 
 // FUSE (H = 256 CTA pairs, configs[3]-sized problems): the rows are not read from HBM. Warps 2-3 of each CTA
@@ -210,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_wo = reinterpret_cast<float*>(smem + C::OFF_WO);
     float* s_b1 = reinterpret_cast<float*>(smem + C::OFF_B1);
     float* s_part = reinterpret_cast<float*>(smem + C::OFF_PART);
+    const float* s_hb = reinterpret_cast<const float*>(smem + C::OFF_HB);   // !BIAS_MMA
     const uint32_t bar0 = sbase + C::OFF_BAR;
     auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
@@ -236,10 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (C::L1M) {
         // layer-1 B operand of this CTA: rows = its RB neurons of each N-half unit, K = 32 columns pairing with
         // the A columns (t = 0..5 per coordinate c, column 3 t + c): w_h, w_m, w_h, w_l, w_m, w_h (x kP)
+        // L1PE: then per PE feature f (columns 18 + 3 f + {0, 1, 2}) the two-part split w_h, w_l, w_h (weights from
+        // the kP-scaled pair-major copy w1pe2)
         for (int idx = threadIdx.x; idx < C::NH * C::RB; idx += kThreads) {
             const int q = idx / C::RB, nn = idx % C::RB;
-            const float4 w = w1p[q * C::UN + (int)rank * C::RB + nn];
-            const float wc[3] = {w.x * kP, w.y * kP, w.z * kP};
+            const int n = q * C::UN + (int)rank * C::RB + nn;   // neuron
+            auto wpe = [&](int f) {   // kP W1[n][f], f < NPE
+                const float2 w2 = w1pe2[(n / 2) * C::NPE + f];
+                return (n & 1) ? w2.y : w2.x;
+            };
+            float wc[3];
+            if constexpr (C::L1PE) {
+                wc[0] = wpe(0); wc[1] = wpe(1); wc[2] = wpe(2);
+            } else {
+                const float4 w = w1p[n];
+                wc[0] = w.x * kP; wc[1] = w.y * kP; wc[2] = w.z * kP;
+            }
             uint16_t part[3][3];   // [h, m, l][c]
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -252,12 +278,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 part[2][c] = __bfloat16_as_ushort(lb);
             }
             constexpr int kB[6] = {0, 1, 0, 2, 1, 0};   // B part of term t
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const uint16_t v = k >= 18 ? (uint16_t)0 : part[kB[k / 3]][k % 3];
+            for (int k = 0; k < C::K1; ++k) {
+                uint16_t v = 0;
+                if (k < 18) {
+                    v = part[kB[k / 3]][k % 3];
+                } else if (k < C::K1_USED) {
+                    const float w = wpe(3 + (k - 18) / 3);
+                    const __nv_bfloat16 hb = __float2bfloat16_rn(w);
+                    v = (k - 18) % 3 == 1 ? __bfloat16_as_ushort(__float2bfloat16_rn(w - __bfloat162float(hb)))
+                                          : __bfloat16_as_ushort(hb);
+                }
                 const int st = k / 16, kk = k % 16;
-                *reinterpret_cast<uint16_t*>(smem + C::OFF_BL1 + (q * 2 + st) * C::BL1_TILE + (nn / 8) * 256 + (kk / 8) * 128 +
-                                             (nn % 8) * 16 + (kk % 8) * 2) = v;
+                *reinterpret_cast<uint16_t*>(smem + C::OFF_BL1 + (q * C::K1S + st) * C::BL1_TILE + (nn / 8) * 256 +
+                                             (kk / 8) * 128 + (nn % 8) * 16 + (kk % 8) * 2) = v;
             }
         }
     } else
@@ -270,6 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2* s_pe = reinterpret_cast<float2*>(smem + C::OFF_PE);
         for (int i = threadIdx.x; i < (H / 2) * C::NPE; i += kThreads) s_pe[i] = w1pe2[i];
     }
+    if constexpr (!C::BIAS_MMA) {   // hidden biases for the epilogue, kP-scaled fp32
+        float* s_hb = reinterpret_cast<float*>(smem + C::OFF_HB);
+        for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
+    }
+    if constexpr (C::BIAS_MMA)
     for (int r = threadIdx.x; r < kTileRows; r += kThreads) {   // ones tile: row r = [1, 1, 0 x 14] (bf16)
         uint32_t* o = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (r / 8) * 256 + (r % 8) * 16);
         o[0] = 0x3F803F80u;
@@ -319,12 +357,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 1) {
         // ================= weight loader: this CTA's share of every unit, once
         if (lane == 0 && group < n_tiles) {
-            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)C::IMG_BYTES);
+            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)(C::W_BYTES + C::BIAS_BYTES));
             const uint8_t* src = wimg + (size_t)rank * C::IMG_BYTES;
             for (int u = 0; u < G * C::NH; ++u)
                 bulk_g2s(sbase + (uint32_t)(u * C::UNIT_BYTES), src + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
                          bar(BAR_WLOCAL));
-            bulk_g2s(sbase + (uint32_t)C::OFF_BIAS, src + C::W_BYTES, C::BIAS_BYTES, bar(BAR_WLOCAL));
+            if constexpr (C::BIAS_MMA)
+                bulk_g2s(sbase + (uint32_t)C::OFF_BIAS, src + C::W_BYTES, C::BIAS_BYTES, bar(BAR_WLOCAL));
             mbar_wait(bar(BAR_WLOCAL), 0);
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
             else mbar_arrive_local(bar(BAR_WREADY));
@@ -356,8 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             float part = 0.f;
             for (int t = 0; t < p.T; ++t) {
                 const long long i = j * p.T + t;
-                const int rb = (int)(i % C::NROWBUF);
-                const uint32_t use = (uint32_t)(i / C::NROWBUF);
+                constexpr int kNRB = C::NROWBUF > 0 ? C::NROWBUF : 1;
+                const int rb = (int)(i % kNRB);
+                const uint32_t use = (uint32_t)(i / kNRB);
                 const float4 U = Uo[min(t + sh, p.T - 1)];   // warm-start shift
                 if (first) reinterpret_cast<float4*>(bufs.U_nom)[(long long)bb * p.T + t] = U;
                 float4 n;
@@ -436,17 +476,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                                    (kk / 64) * (kTileRows * 128) + (kk % 64) * 2);
                                         tc_mma_ss<CG>(d_t, smem_desc_sw128(a_addr), smem_desc_sw128(b_addr), idesc, 1u);
                                     } else {
-                                        tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc, 1u);
+                                        tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), smem_desc_sw128(b_addr), idesc,
+                                                  (C::BIAS_MMA || j > 0) ? 1u : 0u);
                                     }
                                 }
                             };
-                            if (C::L1M && l < 0) {   // layer 1: D = A1 (TMEM) x B1^T, K = 32 (bias b1' in the epilogue)
+                            if (C::L1M && l < 0) {   // layer 1: D = A1 (TMEM) x B1^T, K = K1 (bias b1' in the epilogue)
                                 if (!kWarpIssuer || elect_one()) {
 #pragma unroll
-                                    for (int st = 0; st < 2; ++st)
+                                    for (int st = 0; st < C::K1S; ++st)
                                         tc_mma_ts<CG>(d_t, a_t + (uint32_t)(st * 8),
-                                                      smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BL1 + (h * 2 + st) * C::BL1_TILE)),
-                                                      idesc, (uint32_t)st);
+                                                      smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BL1 + (h * C::K1S + st) * C::BL1_TILE)),
+                                                      idesc, st > 0 ? 1u : 0u);
                                     tc_commit<CG>(bar(BAR_MMA + sl));
                                 }
                                 if constexpr (kWarpIssuer) __syncwarp();
@@ -457,9 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int j_mid = C::SPLITK && h == 0 ? H / 32 : H / 16;
                             if (!kWarpIssuer || elect_one()) {
                                 // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
-                                tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
-                                              smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
-                                              idesc, 0u);
+                                if constexpr (C::BIAS_MMA)
+                                    tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
+                                                  smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
+                                                  idesc, 0u);
                                 issue_k(0, j_mid);
                             }
                             if (C::SPLITK && h == 0) {
@@ -519,22 +561,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         // query rows of this CTA's part of tile i -> smem buffer i % NROWBUF by one bulk-async copy (TMA
         // engine), issued one tile of this slot (NSLOT tiles) ahead by one elected thread of the group
         const float4* s_rows = reinterpret_cast<const float4*>(smem + C::OFF_ROWS);
+        constexpr int kNRB = C::NROWBUF > 0 ? C::NROWBUF : 1;   // (no row buffers with L1PE: never used)
         const bool row_issuer = eg == 0 && lane == 0;
         auto issue_rows = [&](long long i) {
-            if (FUSE || !row_issuer || i >= n_my) return;   // FUSE: the rollout warps write the rows
+            if (FUSE || C::NROWBUF == 0 || !row_issuer || i >= n_my) return;   // FUSE: the rollout warps write the rows
             const long long r0 = row0_of(i);
             const long long nv = min((long long)kTileRows, n_rows - r0);
             if (nv <= 0) {
-                mbar_arrive_local(bar(BAR_ROWS + (int)(i % C::NROWBUF)));
+                mbar_arrive_local(bar(BAR_ROWS + (int)(i % kNRB)));
                 return;
             }
-            mbar_expect_tx(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)(16 * nv));
-            bulk_g2s(sbase + C::OFF_ROWS + (uint32_t)((i % C::NROWBUF) * 16 * kTileRows), rows + r0, (uint32_t)(16 * nv),
-                     bar(BAR_ROWS + (int)(i % C::NROWBUF)));
+            mbar_expect_tx(bar(BAR_ROWS + (int)(i % kNRB)), (uint32_t)(16 * nv));
+            bulk_g2s(sbase + C::OFF_ROWS + (uint32_t)((i % kNRB) * 16 * kTileRows), rows + r0, (uint32_t)(16 * nv),
+                     bar(BAR_ROWS + (int)(i % kNRB)));
         };
         auto row_of = [&](long long i) {   // this thread's query row of tile i (after its buffer landed)
             const long long row = row0_of(i) + row_in_tile;
-            return row < n_rows ? s_rows[(i % C::NROWBUF) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
+            return row < n_rows ? s_rows[(i % kNRB) * kTileRows + row_in_tile] : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         // 16 layer-1 activations (bf16x2) of this thread's row, neurons j0..j0+15 -> the slot's A operand:
         // TMEM, or (A1S) the shared-memory tile in the SW128 K-major layout of the weight images
@@ -555,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto layer1 = [&](long long i) {
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
-            mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
+            mbar_wait(bar(BAR_ROWS + (int)(i % kNRB)), (uint32_t)((i / kNRB) & 1));
             if (tracer) TC_TRACE(trole, 11, 0, 0, sl, t1);
             const float4 q = row_of(i);
             const float2 qx2 = make_float2(q.x, q.x), qy2 = make_float2(q.y, q.y), qz2 = make_float2(q.z, q.z);
@@ -587,9 +630,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sincospif(q.z * sc, &feat[3 + 6 * bnd + 2], &feat[3 + 6 * bnd + 5]);
                 }
                 const float2* s_pe = reinterpret_cast<const float2*>(smem + C::OFF_PE);
-                auto pe_w = [&](int idx) {
+                auto pe_w = [&](int idx) -> float2 {
                     if constexpr (C::PE_SMEM) return s_pe[idx];
-                    else return pew.w[idx];
+                    else if constexpr (sizeof(pew) > 1) return pew.w[idx];
+                    else return make_float2(0.f, 0.f);   // L1PE: layer 1 is prep() + an MMA (never called)
                 };
 #pragma unroll
                 for (int c = 0; c < C::NH; ++c) {
@@ -671,17 +715,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
 
-        // L1M: the layer-1 MMA operand of tile i (exact bf16 splits of p_c, K = 32) -> the slot's A columns in
-        // TMEM; the tile's |v| and far-controller state are kept in registers for its epilogues
-        float vn_nx = 0.f;
-        const float* bfar_nx = nullptr;
-        bool any_far_nx = false;
+        // L1M: the layer-1 MMA operand of tile i (exact bf16 splits of p_c, K = 32 or 96) -> the slot's A columns in
+        // TMEM. Nothing of the tile is kept in registers across its layers (the epilogue is at its register limit):
+        // the far-controller state is recomputed in the layer-1 epilogue and |v| re-read at the output.
+        // L1PE: no row buffers -- each thread loads its query row itself (an L2 prefetch is issued a tile ahead)
+        auto row_ptr = [&](long long i) -> const float4* {
+            const long long row = row0_of(i) + row_in_tile;
+            return i < n_my && row < n_rows ? rows + row : nullptr;
+        };
         auto prep = [&](long long i) {
             const long long t1 = tile_of(i);
             if (tracer) TC_TRACE(trole, 6, 0, 0, sl, t1);
-            mbar_wait(bar(BAR_ROWS + (int)(i % C::NROWBUF)), (uint32_t)((i / C::NROWBUF) & 1));
-            const float4 q = row_of(i);
-            vn_nx = q.w;
+            float4 q;
+            if constexpr (C::L1PE) {
+                const float4* rp = row_ptr(i);
+                q = rp ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                mbar_wait(bar(BAR_ROWS + (int)(i % kNRB)), (uint32_t)((i / kNRB) & 1));
+                q = row_of(i);
+            }
             const long long row0 = tile_row0(t1);
             const long long lo = states_mode ? ctrl_of(min(row0, n_rows - 1)) : ctrl_fixed;
             if (lo != staged) {   // uniform across the group; b1g of the previous tile is no longer read
@@ -689,10 +741,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = gtid; j < H; j += gthreads) b1g[j] = lo < p.n_ctrl ? b1f[(size_t)lo * H + j] * kP : 0.f;
                 staged = lo;
             }
-            const long long row = row0 + row_in_tile;
-            const long long bb = states_mode ? ctrl_of(min(row, n_rows - 1)) : ctrl_fixed;
-            bfar_nx = bb != lo ? b1f + (size_t)bb * H : nullptr;
-            any_far_nx = __any_sync(0xFFFFFFFFu, bfar_nx != nullptr);
             uint32_t hv[3], mv[3], lv[3];
             const float pc[3] = {q.x, q.y, q.z};
 #pragma unroll
@@ -718,10 +766,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 kv[w2] = v2[0] | (v2[1] << 16);
             }
-            uint32_t a[8];
+            const uint32_t a_base = tmem + lane_addr + (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
+            if constexpr (C::L1PE) {
+                // columns 18 + 3 f + {0, 1, 2} = f_h, f_h, f_l per PE feature f (pairs with B: w_h, w_l, w_h); f = 6 b + c
+                // (sin), 6 b + 3 + c (cos); each of the row's two threads writes 24 of the 48 TMEM columns
+                auto feat = [&](int f) -> float {   // PE feature f (compile-time): sin / cos(2^b pi p_c), f = 6 b + 3 cos + c
+                    float sv, cv;
+                    sincospif(pc[f % 3] * (float)(1 << (f / 6)), &sv, &cv);
+                    return (f % 6) >= 3 ? cv : sv;
+                };
+                auto colv = [&](int k) -> uint32_t {   // bf16 bits of operand column k (compile-time k)
+                    if (k < 18) {
+                        const int t = k / 3, c = k % 3;
+                        return (t == 2 || t == 4) ? mv[c] : t == 5 ? lv[c] : hv[c];
+                    }
+                    if (k >= C::K1_USED) return 0u;
+                    const float fv = feat((k - 18) / 3);
+                    const __nv_bfloat16 fh = __float2bfloat16_rn(fv);
+                    if ((k - 18) % 3 < 2) return __bfloat16_as_ushort(fh);
+                    return __bfloat16_as_ushort(__float2bfloat16_rn(fv - __bfloat162float(fh)));
+                };
+                constexpr int kHalf = C::K1 / 4;   // TMEM columns (bf16 pairs) per thread: 24
+                auto store_half = [&](auto cg_c) {   // this thread's 24 columns, 8 at a time (features computed per store)
+                    constexpr int cg = decltype(cg_c)::value;
 #pragma unroll
-            for (int w2 = 0; w2 < 8; ++w2) a[w2] = cgi == 0 ? kv[w2] : kv[8 + w2];
-            tmem_st8(tmem + lane_addr + (uint32_t)(sl * C::SLOT_COLS + C::A_OFF + 8 * cgi), a);
+                    for (int s8 = 0; s8 < kHalf / 8; ++s8) {
+                        uint32_t a8[8];
+#pragma unroll
+                        for (int w2 = 0; w2 < 8; ++w2) {
+                            const int k = 2 * (kHalf * cg + 8 * s8 + w2);
+                            a8[w2] = colv(k) | (colv(k + 1) << 16);
+                        }
+                        tmem_st8(a_base + (uint32_t)(kHalf * cg + 8 * s8), a8);
+                    }
+                };
+                if (cgi == 0) store_half(std::integral_constant<int, 0>{});
+                else store_half(std::integral_constant<int, 1>{});
+            } else {
+                uint32_t a[8];
+#pragma unroll
+                for (int w2 = 0; w2 < 8; ++w2) a[w2] = cgi == 0 ? kv[w2] : kv[8 + w2];
+                tmem_st8(a_base + (uint32_t)(8 * cgi), a);
+            }
             named_bar_sync(1 + C::NSLOT + sl, gthreads);   // every warp has read the row buffer (and b1g is staged)
             issue_rows(i + C::NSLOT);
             tmem_wait_st();
@@ -730,9 +816,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) arrive_sched(BAR_AREADY + sl);
             if (tracer) TC_TRACE(trole, 7, 0, 0, sl, t1);
         };
-        float vn = 0.f;
-        const float* bfar_t = nullptr;
-        bool any_far_t = false;
         issue_rows(sl);
         if constexpr (C::L1M) {
             if (sl < n_my) prep(sl);
@@ -743,22 +826,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (long long i = sl; i < n_my; i += C::NSLOT) {
             uint32_t keep[C::NH > 1 ? C::QW / 2 : 1];   // unit-0 activations (bf16x2) until unit 1 is done
             float2 sdot2 = make_float2(0.f, 0.f);
-            if constexpr (C::L1M) {
-                vn = vn_nx;
-                bfar_t = bfar_nx;
-                any_far_t = any_far_nx;
+            if constexpr (C::L1PE) {   // the row prep(i + NSLOT) reads, into L2 a tile ahead
+                const float4* rp = row_ptr(i + C::NSLOT);
+                if (rp) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
             }
-#pragma unroll 1
-            for (int l = C::L1M ? -1 : 0; l < G; ++l) {
-                const bool last = (l == G - 1);
+            // one layer's units; layer 1 (L1M) is a separate instantiation (kL1), so its epilogue's registers are
+            // allocated apart from the GEMM layers' rolled loop
+            auto run_layer = [&](auto l1c, const int l) {
+                constexpr bool kL1 = decltype(l1c)::value;
+                const bool last = !kL1 && (l == G - 1);
 #pragma unroll
                 for (int h = 0; h < C::NH; ++h) {
                     if (tracer) TC_TRACE(trole, 3, l, h, sl, i);
                     mbar_wait(bar(BAR_MMA + sl), (mma_cnt++) & 1);
                     tc_fence_after();
                     if (tracer) TC_TRACE(trole, 4, l, h, sl, i);
-                    // L1M: the tile's last MMA has read A -> next tile's layer-1 operand into the dead A columns
-                    if (C::L1M && last && h == C::NH - 1 && i + C::NSLOT < n_my) prep(i + C::NSLOT);
                     const uint32_t d_col = (uint32_t)(sl * C::SLOT_COLS + cgi * C::QW);
                     const uint32_t a_col = (uint32_t)(sl * C::SLOT_COLS + C::A_OFF);
                     if (C::SPLITK && !last && h == C::NH - 1) {
@@ -771,12 +853,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) arrive_sched(BAR_AK0 + sl);
                     }
+                    // L1M: the tile's last MMA has read A -> next tile's layer-1 operand into the dead A columns (after
+                    // the keep[] store above, so keep[] is dead here: prep's registers do not spill it)
+                    if (C::L1M && last && h == C::NH - 1 && i + C::NSLOT < n_my) prep(i + C::NSLOT);
                     // H = 256: chunk k + 1's TMEM load is in flight while chunk k is computed (configs[2] -2%;
                     // H = 128 +2%: load, wait, compute)
                     // kAll (H = 256): the whole D share of the warp (NCH x 16 columns) loaded at once, one wait, and
                     // D released before any of it is computed, so the slot's next unit can start ~1 k cycles
                     // earlier (the N-half-0 activations kept in registers are already stored at h = 1)
-                    constexpr bool kAll = MPPI_EPI_ALL < 0 ? CG == 2 : MPPI_EPI_ALL != 0;
+                    // (L1M: off -- with layer 1's epilogue and prep in the same loop, kAll's 64 live accumulator registers
+                    // spill the tile state; the pipelined form has no spills)
+                    constexpr bool kAll = MPPI_EPI_ALL < 0 ? CG == 2 && !C::L1M : MPPI_EPI_ALL != 0;
                     constexpr bool kPipe = !kAll && (MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0);
                     uint32_t accb[kAll ? C::NCH : kPipe ? 2 : 1][kCW];
                     if constexpr (kAll) {
@@ -808,7 +895,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int j0 = h * C::UN + cgi * C::QW + k * kCW;   // output neuron index
                         if (!last) {
                             uint32_t packed[kCW / 2];
-                            if (C::L1M && l < 0) {   // layer 1: D + kP b1' (per controller), fast path for one controller
+                            if (kL1) {   // layer 1: D + kP b1' (per controller), fast path for one controller
+                                // rows of a controller after the staged one (the tile crosses a controller boundary)
+                                const long long row = row0_of(i) + row_in_tile;
+                                const long long bb = states_mode ? ctrl_of(min(row, n_rows - 1)) : ctrl_fixed;
+                                const float* bfar_t = bb != staged ? b1f + (size_t)bb * H : nullptr;
+                                const bool any_far_t = __any_sync(0xFFFFFFFFu, bfar_t != nullptr);
                                 if (!any_far_t) {
 #pragma unroll
                                     for (int i2 = 0; i2 < kCW; i2 += 4) {
@@ -828,6 +920,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         packed[i2 / 2] = act_pack<ACT>(__uint_as_float(acc[i2]) + b0, __uint_as_float(acc[i2 + 1]) + b1);
                                     }
                                 }
+                            } else if constexpr (!C::BIAS_MMA) {
+#pragma unroll
+                            for (int i2 = 0; i2 < kCW; i2 += 4) {   // D = kP W a; + kP b (fp32) here
+                                const float4 bv = *reinterpret_cast<const float4*>(s_hb + l * H + j0 + i2);
+                                const float2 x0 = ffma2(make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1])),
+                                                        make_float2(1.f, 1.f), make_float2(bv.x, bv.y));
+                                const float2 x1 = ffma2(make_float2(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3])),
+                                                        make_float2(1.f, 1.f), make_float2(bv.z, bv.w));
+                                packed[i2 / 2] = act_pack<ACT>(x0.x, x0.y);
+                                packed[i2 / 2 + 1] = act_pack<ACT>(x1.x, x1.y);
+                            }
                             } else {
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
@@ -849,8 +952,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int i2 = 0; i2 < kCW; i2 += 4) {
                                 const float4 wv = *reinterpret_cast<const float4*>(s_wo + j0 + i2);
-                                const uint32_t p0 = act_pack<ACT>(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]));
-                                const uint32_t p1 = act_pack<ACT>(__uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3]));
+                                float4 xv = make_float4(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]),
+                                                        __uint_as_float(acc[i2 + 2]), __uint_as_float(acc[i2 + 3]));
+                                if constexpr (!C::BIAS_MMA) {   // + kP b of the last hidden layer
+                                    const float4 bv = *reinterpret_cast<const float4*>(s_hb + l * H + j0 + i2);
+                                    const float2 x0 = ffma2(make_float2(xv.x, xv.y), make_float2(1.f, 1.f), make_float2(bv.x, bv.y));
+                                    const float2 x1 = ffma2(make_float2(xv.z, xv.w), make_float2(1.f, 1.f), make_float2(bv.z, bv.w));
+                                    xv = make_float4(x0.x, x0.y, x1.x, x1.y);
+                                }
+                                const uint32_t p0 = act_pack<ACT>(xv.x, xv.y);
+                                const uint32_t p1 = act_pack<ACT>(xv.z, xv.w);
                                 // output dot in two interleaved partial sums (even / odd neurons)
                                 sdot2 = ffma2(make_float2(__uint_as_float(p0 << 16), __uint_as_float(p0 & 0xFFFF0000u)),
                                               make_float2(wv.x, wv.y), sdot2);
@@ -867,6 +978,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (tracer) TC_TRACE(trole, 5, l, h, sl, i);
                 }
+            };
+            if constexpr (C::L1M) run_layer(std::true_type{}, -1);
+#pragma unroll 1
+            for (int l = 0; l < G; ++l) {
+                run_layer(std::false_type{}, l);
                 if constexpr (C::A1S)   // the first GEMM has read the smem A tile: next tile's layer 1
                     if (l == 0 && i + C::NSLOT < n_my) layer1(i + C::NSLOT);
             }
@@ -884,7 +1000,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.rps == 2) {
                         const float s1 = __shfl_xor_sync(0xFFFFFFFFu, sv, 1);
                         const float term = p.w_sdf * __expf(fminf(-sv * p.inv_sdf_scale, p.sdf_exp_max)) -
-                                           p.w_guide * (C::L1M ? vn : row_of(i).w) * (s1 - sv) * p.inv_fd_h;
+                                           p.w_guide *
+                                               (C::L1M ? (row < n_rows ? __ldg(reinterpret_cast<const float*>(rows + row) + 3) : 0.f)
+                                                       : row_of(i).w) *
+                                               (s1 - sv) * p.inv_fd_h;
                         if ((lane & 1) == 0 && row < n_rows) terms[row >> 1] = term;
                     } else {
                         const float term = p.model == MPPI_MODEL_PAPER
@@ -895,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             named_bar_sync(1 + sl, gthreads);   // part[] and the row buffer are reused by this group
-            if (FUSE && row_issuer) mbar_arrive_local(bar(BAR_RFREE + (int)(i % C::NROWBUF)));   // to the rollout warps
+            if (FUSE && row_issuer) mbar_arrive_local(bar(BAR_RFREE + (int)(i % kNRB)));   // to the rollout warps
             if (tracer) TC_TRACE(trole, 8, 0, 0, sl, i);
             if constexpr (C::L1M) {
             } else if constexpr (C::A1S) issue_rows(i + 2 * C::NSLOT);   // this tile's row buffer is free now
@@ -1056,7 +1175,8 @@ cudaError_t launch_mlp_tc(const Params& p, const Buffers& b, const float4* rows,
 #define MPPI_TC_FUSE(GG, AA) \
         if (p.H == 256 && p.n_gemm == GG && p.act == AA && p.pe_bands == 0) \
             return tc::launch_t<256, GG, AA, 0, true>(p, b, rows, n_rows, ctrl_fixed, sdf_out, states_mode, s);
-#ifdef MPPI_TC_QUICK
+#if MPPI_L1_MMA   // (the fused producer runs beside the CUDA-core layer 1 only)
+#elif defined(MPPI_TC_QUICK)
         MPPI_TC_FUSE(3, 2)
 #else
         MPPI_TC_FUSE(3, 1) MPPI_TC_FUSE(3, 2)
