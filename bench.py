@@ -411,7 +411,8 @@ def main():
     ctrl.close()
     if world == 1 and not args.no_extra and args.config == "auto":
         # driver-observed figures for the other configurations in the same invocation:
-        # north_star's target (configs[2] < 1 ms on one B200) and configs[1], [4] and the paper-model c5
+        # north_star's target (configs[2] < 1 ms on one B200) and configs[1], [4], the paper-model c5 and the
+        # positional-encoding variants of the configs[1] / configs[2] MLPs
         ns = extra_line("c2", max(args.steps, 20), args.warmup, local, peaks)
         ns.update({"target_ms": 1.0, "target_met": ns["ms_per_step"] < 1.0,
                    "tensor_pipe_pct_ncu": (json.load(open(os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")))
@@ -421,7 +422,7 @@ def main():
                                        "never a number taken under the profiler for time"})
         line["north_star_c2"] = ns
         line["other_configs"] = {n: extra_line(n, max(args.steps, 20), args.warmup, local, peaks)
-                                 for n in ("c1", "c4", "c5")}
+                                 for n in ("c1", "c4", "c5", "c1pe", "c2pe")}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)[0]
         try:

@@ -93,6 +93,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_L1_MMA
 #define MPPI_L1_MMA 0   // H = 256: layer 1 as a K = 32 MMA on exact bf16 splits (see Cfg::L1M; A/B: +28% at configs[2])
 #endif
+#ifndef MPPI_L1M_ALL
+#define MPPI_L1M_ALL 0   // L1M: the GEMM layers' epilogues load the whole D share at once (kAll), layer 1 pipelined
+#endif
 #ifndef MPPI_PE_MMA
 #define MPPI_PE_MMA 1   // H = 256 with PE: the 27 position features as a K = 96 exact-split MMA (Cfg::L1PE)
 #endif
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // earlier (the N-half-0 activations kept in registers are already stored at h = 1)
                     // (L1M: off -- with layer 1's epilogue and prep in the same loop, kAll's 64 live accumulator registers
                     // spill the tile state; the pipelined form has no spills)
-                    constexpr bool kAll = MPPI_EPI_ALL < 0 ? CG == 2 && !C::L1M : MPPI_EPI_ALL != 0;
+                    constexpr bool kAll = MPPI_EPI_ALL < 0 ? CG == 2 && (!C::L1M || (MPPI_L1M_ALL && !kL1)) : MPPI_EPI_ALL != 0;
                     constexpr bool kPipe = !kAll && (MPPI_EPI_PIPE < 0 ? CG == 2 : MPPI_EPI_PIPE != 0);
                     uint32_t accb[kAll ? C::NCH : kPipe ? 2 : 1][kCW];
                     if constexpr (kAll) {
