@@ -9,12 +9,12 @@ nvidia-smi --query-gpu=name,driver_version,clocks.max.sm --format=csv,noheader >
 lscpu | grep -E "^CPU\(s\)|Model name" > $O/cpu.txt
 timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench_c3.json 2> $O/bench_c3.err   # the default line (+ c2/c1/c4/c5 keys)
 cp gpurun_out/clocks_rank0.csv $O/clocks_last_run.csv
-for c in c1pe; do timeout 300 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; done
+for c in c1pe c2pe; do timeout 300 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > $O/plain.log 2>&1 && \
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/ncu_launches_c3.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > $O/ncu_launch.log 2>&1
-for c in c3 c2 c1 c4; do
+for c in c3 c2 c1 c4 c2pe; do
   python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/plain_$c.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mlp -s 4 -c 1 -o $O/mlp_$c \
     python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_mlp_$c.log 2>&1

@@ -51,7 +51,7 @@ def main():
     summ_path = os.path.join(dst, "..", "ncu_mlp_summary.json") if len(sys.argv) > 3 else \
         os.path.join(ROOT, "profiles", "ncu_mlp_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    for c in ["c3", "c2", "c1", "c4"]:
+    for c in ["c3", "c2", "c1", "c4", "c2pe"]:
         rep = os.path.join(src, f"mlp_{c}.ncu-rep")
         if not os.path.exists(rep):
             continue
