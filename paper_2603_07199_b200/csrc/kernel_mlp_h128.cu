@@ -68,6 +68,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_STAG
 #define H128_STAG 0   // > 0: staggered issue order (slot s starts H128_STAG * s visits late)
 #endif
+#ifndef H128_L1LAG
+#define H128_L1LAG 4   // issue order: the next round's layer-1 unit of slot s follows the last GEMM of slot s + LAG
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -476,11 +479,25 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                 if (!any) break;
             }
 #else
+            // lockstep rounds: per round of NS tiles, unit u of every slot before unit u + 1. The next round's
+            // layer-1 units are interleaved into this round's last GEMM units, slot s's right after the last GEMM
+            // of slot s + H128_L1LAG (H128_L1LAG >= NS: all of them after the last GEMMs, the plain order), so the
+            // small layer-1 MMAs and their epilogues overlap the other slots' last GEMMs
+            constexpr int kLag = H128_L1LAG;
+            {
+                const int ns0 = (int)min((long long)NS, n_my);
+                for (int sl = 0; sl < ns0; ++sl) issue_unit(sl, 0, 0u, 0);
+            }
             for (long long i0 = 0; i0 < n_my; i0 += NS) {
                 const uint32_t n = (uint32_t)(i0 / NS);
                 const int ns = (int)min((long long)NS, n_my - i0);
-                for (int u = 0; u <= G; ++u)
+                const int ns_next = (int)max(0ll, min((long long)NS, n_my - i0 - NS));
+                for (int u = 1; u < G; ++u)
                     for (int sl = 0; sl < ns; ++sl) issue_unit(sl, u, n, i0);
+                for (int j = 0; j < ns || j - kLag < ns_next; ++j) {
+                    if (j < ns) issue_unit(j, G, n, i0);
+                    if (j - kLag >= 0 && j - kLag < ns_next) issue_unit(j - kLag, 0, n + 1, i0 + NS);
+                }
             }
 #endif
         }
