@@ -446,3 +446,71 @@ def test_largest_problem_sampled_costs(base):
     assert np.isfinite(Ug).all()
     assert (Ug >= np.array(cfg.u_lo) - 1e-4).all() and (Ug <= np.array(cfg.u_hi) + 1e-4).all()
     ctrl.close()
+
+
+# ---------------------------------------------------------------- positional encoding: constructed network
+
+def _pe_abs_net(cfg):
+    """An exact ReLU network over the 27 PE(p) features (reading E1): layer 1 neurons 2f, 2f+1 = relu(+-PE_f(p)),
+    layer 2 neuron f = |PE_f| (two unit weights), later hidden layers identity, output c + sum_f w_f |PE_f| with
+    distinct w_f = (f + 1) / 32 (exact in bf16). Every feature has its own output weight, so a PE column placed
+    at the wrong K offset, a swapped sin / cos or a wrong band changes the result by O(0.1)."""
+    npe = 3 + 6 * cfg.pe_bands
+    Ws = [np.zeros((o, i), np.float32) for (i, o) in cfg.layer_dims]
+    bs = [np.zeros((o,), np.float32) for (i, o) in cfg.layer_dims]
+    for f in range(npe):
+        Ws[0][2 * f, f] = 1.0
+        Ws[0][2 * f + 1, f] = -1.0
+        Ws[1][f, 2 * f] = Ws[1][f, 2 * f + 1] = 1.0
+    for l in range(2, cfg.n_hidden):
+        for f in range(npe):
+            Ws[l][f, f] = 1.0
+    wf = (np.arange(npe) + 1) / 32.0
+    Ws[-1][0, :npe] = wf
+    bs[-1][0] = 0.25
+    return Ws, bs, wf
+
+
+@pytest.mark.parametrize("name", ["c1pes", "c2pes"])
+def test_tc_pe_constructed_net(name):
+    """The positional-encoding layer 1 on the tensor cores (K = 96 exact-split MMA at H = 128 and, since the final
+    round-2 session, at H = 256) against a closed form: s = c + sum_f w_f |PE_f(p)| with PE written out here in
+    float64 (sin / cos(2^b pi p), reading E1). Oracle parity: the only rounding in the network is
+    R15's bf16 rounding of the layer-1 activations |PE_f| (every later product and sum is exact), so a row differs
+    from the oracle only where the kernel's fp32 feature (sincospif, two-part split: <= 2^-16 relative, reading E2)
+    and the oracle's float64 one round to different bf16 neighbours: one ulp of |PE_f| per flip, on few rows."""
+    cfg = synth.get_config(name, activation=synth.configs.ACT_RELU)
+    Ws, bs, wf = _pe_abs_net(cfg)
+    cfg, _, _, inp, ctrl = gh.setup(name, weights=(Ws, bs), activation=synth.configs.ACT_RELU)
+    cg = 2 if cfg.hidden == 256 else 1
+    rows = synth.make_query_rows(128 * cg * 9 + 77, scale=1.7, seed=21)   # several tiles + a ragged tail
+    got = ctrl.sdf_eval(rows, ctrl=0).cpu().numpy().astype(np.float64)
+    ref = oracle.sdf_rows(oracle.make_cfg(cfg), Ws, bs, inp["z"][0], rows)
+    p = rows[:, :3].astype(np.float64)
+    feats = [p[:, 0], p[:, 1], p[:, 2]]
+    for b in range(cfg.pe_bands):
+        feats += [np.sin(2.0 ** b * np.pi * p[:, c]) for c in range(3)]
+        feats += [np.cos(2.0 ** b * np.pi * p[:, c]) for c in range(3)]
+    F = np.abs(np.stack(feats, 1))
+    closed = 0.25 + F @ wf
+    ulp = 2.0 ** (np.floor(np.log2(np.maximum(F, 2.0 ** -30))) - 7)   # bf16 ulp of each |PE_f|
+    # closed form within R15's rounding of every layer-1 activation (half an ulp each)
+    assert np.all(np.abs(got - closed) <= (0.5 * ulp) @ wf + 1e-6)
+    # oracle: exact except on rows with flipped bf16 roundings (each flip one ulp of one feature)
+    d = np.abs(got - ref)
+    assert np.all(d <= ulp @ wf + 1e-6), d.max()
+    assert (d > 1e-6).mean() <= 0.05, (d > 1e-6).mean()
+
+
+@pytest.mark.parametrize("name", ["c2s", "c2pes"])
+def test_h256_step_across_controllers(name):
+    """H = 256 (CTA-pair tiles of 256 rows) with three controllers of 136 x 5 x 2 = 1360 rows each: pair tiles
+    straddle controller boundaries, so the layer-1 epilogue's far-controller path (a row whose folded bias b1'
+    belongs to a later controller than the staged one) runs -- for the CUDA-core layer 1 (c2s) and the
+    positional-encoding MMA layer 1 (c2pes). Per-controller latents, gates and goals."""
+    from tests.test_gpu_parity import _bf16_step_checks
+    cfg, Ws, bs, inp, ctrl = gh.setup(name, n_ctrl=3)
+    assert (cfg.K * cfg.T * 2) % 256 != 0
+    ctrl.step(inp["x0"], inp["goal"], 0)
+    ref = gh.run_oracle(cfg, Ws, bs, inp)
+    _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
