@@ -71,6 +71,11 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef H128_L1LAG
 #define H128_L1LAG 4   // issue order: the next round's layer-1 unit of slot s follows the last GEMM of slot s + LAG
 #endif
+#ifndef H128_DESC_ADD
+#define H128_DESC_ADD 1   // GEMM K-step descriptors by one 32-bit add on the address field (0: rebuilt per MMA;
+                          // measured -1.7% at configs[4], -1.6% at configs[1]: the issuer shares SMSP 0 with 4 busy
+                          // epilogue warps, so its instruction count per unit is on the MMA hand-off path)
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -398,11 +403,25 @@ __global__ void __launch_bounds__(Cfg<G, PEB, FUSE>::THREADS, 1)
                                      idesc, 0u);
 #endif
                         const uint32_t w0 = sbase + (uint32_t)(l * H * H * 2);
+#if H128_DESC_ADD
+                        // K step j: the descriptors' 14-bit address fields advance by off / 16 (no carry: shared
+                        // addresses < 256 KB), so one 32-bit add per operand instead of a descriptor rebuild
+                        const uint64_t ad = smem_desc_sw128(a0), wd = smem_desc_sw128(w0);
+                        const uint32_t ad_lo = (uint32_t)ad, ad_hi = (uint32_t)(ad >> 32);
+                        const uint32_t wd_lo = (uint32_t)wd, wd_hi = (uint32_t)(wd >> 32);
+#pragma unroll
+                        for (int j = 0; j < H / 16; ++j) {
+                            const uint32_t o16 = (uint32_t)((j / 4) * (kRows * 128) + (j % 4) * 32) >> 4;
+                            tc_mma_ss<1>(d_t, ((uint64_t)ad_hi << 32) | (ad_lo + o16), ((uint64_t)wd_hi << 32) | (wd_lo + o16),
+                                         idesc, 1u);
+                        }
+#else
 #pragma unroll
                         for (int j = 0; j < H / 16; ++j) {
                             const uint32_t off = (uint32_t)((j / 4) * (kRows * 128) + (j % 4) * 32);
                             tc_mma_ss<1>(d_t, smem_desc_sw128(a0 + off), smem_desc_sw128(w0 + off), idesc, 1u);
                         }
+#endif
                     }
                     tc_commit<1>(bar(BAR_MMA + sl));
                     // a second commit of the last GEMM for the layer-1 builder (its own barrier: waiting on

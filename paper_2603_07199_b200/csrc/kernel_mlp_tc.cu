@@ -96,6 +96,10 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_L1M_ALL
 #define MPPI_L1M_ALL 0   // L1M: the GEMM layers' epilogues load the whole D share at once (kAll), layer 1 pipelined
 #endif
+#ifndef MPPI_DESC_ADD
+#define MPPI_DESC_ADD -1   // TS-form K-step B descriptors by one 32-bit add on the address field: -1 = with PE only
+                          // (A/B: configs[2]+PE -1.5%, configs[2] +0.3%, configs[3] -0.2%), 0 / 1 = off / on
+#endif
 #ifndef MPPI_PE_MMA
 #define MPPI_PE_MMA 1   // H = 256 with PE: the 27 position features as a K = 96 exact-split MMA (Cfg::L1PE)
 #endif
@@ -468,12 +472,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t d_t = tmem + (uint32_t)(sl * C::SLOT_COLS);
                             const uint32_t a_t = d_t + (uint32_t)C::A_OFF;
                             const uint32_t b_unit = sbase + (uint32_t)((l * C::NH + h) * C::UNIT_BYTES);
+                            // the B descriptor of K step j is the unit's with its 14-bit address field advanced by the byte
+                            // offset / 16 (no carry: shared addresses < 256 KB): one 32-bit add instead of a rebuild
+                            constexpr bool kDescAdd = MPPI_DESC_ADD < 0 ? C::L1PE : MPPI_DESC_ADD != 0;
+                            const uint64_t bd0 = smem_desc_sw128(b_unit);
+                            const uint32_t bd_lo = (uint32_t)bd0, bd_hi = (uint32_t)(bd0 >> 32);
                             auto issue_k = [&](int j_lo, int j_hi) {   // K steps [16 j_lo, 16 j_hi) of the unit
 #pragma unroll
                                 for (int j = 0; j < H / 16; ++j) {
                                     if (j < j_lo || j >= j_hi) continue;
                                     const int kk = j * 16;
                                     const uint32_t b_addr = b_unit + (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2);
+                                    if (kDescAdd && !a_smem) {
+                                        const uint32_t o16 = (uint32_t)((kk / 64) * (C::RB * 128) + (kk % 64) * 2) >> 4;
+                                        tc_mma_ts<CG>(d_t, a_t + (uint32_t)(kk / 2), ((uint64_t)bd_hi << 32) | (bd_lo + o16), idesc,
+                                                      (C::BIAS_MMA || j > 0) ? 1u : 0u);
+                                        continue;
+                                    }
                                     if (a_smem) {
                                         const uint32_t a_addr = sbase + (uint32_t)(C::OFF_SA + sl * C::SA_BYTES +
                                                                                    (kk / 64) * (kTileRows * 128) + (kk % 64) * 2);
