@@ -76,6 +76,10 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
                           // measured -1.7% at configs[4], -1.6% at configs[1]: the issuer shares SMSP 0 with 4 busy
                           // epilogue warps, so its instruction count per unit is on the MMA hand-off path)
 #endif
+#ifndef H128_WAIT_FIRST
+#define H128_WAIT_FIRST 1   // the issuer probes a barrier once (test_wait) before its try_wait loop (A/B: configs[4]
+                            // -1.1%, configs[1] -0.4%; 0: the loop alone)
+#endif
 #ifndef H128_ISSUER_WAIT
 #define H128_ISSUER_WAIT 0   // 0: try_wait loop (no sleep); 1: try_wait with the 100 ns suspend hint (NANOSLEEP in SASS)
 #endif
@@ -170,6 +174,9 @@ __device__ __forceinline__ void issuer_wait(uint32_t bar, uint32_t parity) {
 #if H128_ISSUER_WAIT == 1
     mbar_wait_issuer(bar, parity);
 #else
+#if H128_WAIT_FIRST
+    if (mbar_test(bar, parity)) return;   // ready: no loop head (YIELD) on the issuer's path
+#endif
     uint32_t n = 0;
     while (!mbar_try_wait<false>(bar, parity))
         if (++n > (1u << 26)) __trap();

@@ -61,12 +61,18 @@ __device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
         : "=r"(ok) : "r"(a), "r"(parity) : "memory");
     return ok != 0;
 }
+#ifndef MPPI_WAIT_FIRST
+#define MPPI_WAIT_FIRST 0   // 1: mbar_wait_issuer probes once (test_wait) before its try_wait loop
+#endif
 #ifndef MPPI_ISSUER_HINT_NS
 #define MPPI_ISSUER_HINT_NS 100
 #endif
 // Issuer-side wait: try_wait with a 100 ns suspend-time hint (measured 3% faster than the default hint
 // at configs[2]; MPPI_ISSUER_SPIN: spin on test_wait).
 __device__ __forceinline__ void mbar_wait_issuer(uint32_t a, uint32_t parity) {
+#if MPPI_WAIT_FIRST
+    if (mbar_test(a, parity)) return;   // ready: no suspend-hint loop on the issuer's path
+#endif
     uint32_t n = 0;
 #if defined(MPPI_ISSUER_SPIN)
     while (!mbar_test(a, parity))
