@@ -300,6 +300,7 @@ def extra_line(name, steps, warmup, local, peaks):
     plan = shard.plan(cfg, 1, 0)
     r = time_config(cfg, plan, 1, 0, local, None, steps, warmup, with_e2e=False)
     rf = roofline_of(cfg, r["lcfg"], r["mlp_ms"], r["ms_per_step"], peaks)
+    fused = bool(r["ctrl"].fused_rollout())
     r["ctrl"].close()
     units = cfg.n_ctrl * cfg.K * cfg.T
     d = {"workload": workload_name(cfg, 1), "ms_per_step": r["ms_per_step"],
@@ -310,7 +311,9 @@ def extra_line(name, steps, warmup, local, peaks):
          "tensor_floor_ms": rf["tensor_floor_ms"], "mlp_share_of_step": rf["mlp_share"],
          "stage_ms": {k: float(v) for k, v in zip(["noise_shift(fused)", "rollout", "sdf_mlp", "softmin_update",
                                                    "exchange"], r["stage_kt"])},
-         "clocks": r["clocks"], "steps": steps, "warmup": warmup}
+         "clocks": r["clocks"], "steps": steps, "warmup": warmup, "fused_rollout": fused}
+    if fused:   # the SDF-MLP launch also runs the rollout (the query rows never reach HBM): its time includes it
+        d["sdf_mlp_note"] = "fused rollout: sdf_mlp_ms is the SDF-MLP kernel that also rolls out (no k_rollout launch)"
     if cfg.n_ctrl > 1:
         d["controller_iterations_per_s"] = cfg.n_ctrl / (r["ms_per_step"] * 1e-3)
     return d
@@ -371,7 +374,11 @@ def main():
     traffic = ncu_traffic(cfg.name)
     # denominator: the SUSTAINED measured bf16 peak -- the launch is timed inside the K-step loop (back-to-back
     # steps, ~0.5 s of load, sw_power_cap active), B200_PROFILING.md's case for it; the burst fraction beside it
-    roofline = {"bound": "tensor", "kernel": "k_mlp_tc (fused SDF-MLP, tcgen05)", "achieved": rf["achieved"],
+    kname = ("k_mlp_tc (fused SDF-MLP, tcgen05, CTA pairs)" if cfg.hidden == 256
+             else "k_mlp_h128 (fused SDF-MLP, tcgen05)")
+    if ctrl.fused_rollout():
+        kname += " with the rollout fused in (its launch time includes the rollout)"
+    roofline = {"bound": "tensor", "kernel": kname, "achieved": rf["achieved"],
                 "peak": peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), "unit": "TFLOP/s",
                 "frac": rf["frac_sustained"], "peak_burst": peaks["bf16_tflops"], "frac_burst": rf["frac"],
                 "peak_source": (f"{peak_src} bf16 dense, sustained (the SDF-MLP launch is timed inside the K-step "

@@ -26,7 +26,7 @@ mppi_status fail(mppi_status st, const std::string& msg) {
 
 constexpr int kStaging = 4;
 // the fused rollout is opt-in (MPPI_FUSED=1); these switch it on by default for large problems
-constexpr bool kFuse128Default = false;
+constexpr bool kFuse128Default = true;    // configs[4]: -0.35% device, -1.2% end to end, -1.68 GB DRAM per step
 constexpr bool kFuse256Default = false;
 constexpr int kNumStages = 5;   // noise+shift, rollout, mlp, cost, update
 
@@ -342,9 +342,10 @@ mppi_status mppi_create(const mppi_config* cfg, void* d_ws, size_t ws_bytes, mpp
         const bool e128 = common && cfg->hidden == 128 && cfg->K % 64 == 0 && !p.mlp_legacy;
         const bool e256 = common && cfg->hidden == 256 && cfg->K % 128 == 0 && cfg->n_hidden == 4 &&
                           (cfg->activation == MPPI_ACT_SILU || cfg->activation == MPPI_ACT_RELU);
-        // default off: configs[4] (H = 128) runs the same step time fused (with 1.68 GB less DRAM traffic) and
-        // configs[3] (H = 256) 2% slower; kFuse128Default / kFuse256Default switch the large-problem
-        // defaults on (>= 8 blocks per SM / CTA pair)
+        // default: on for large H = 128 problems (configs[4]: -0.35% step, -1.2% end to end, 1.68 GB less DRAM
+        // traffic per step; final round-2 session A/B), off at H = 256 (configs[3] 2% slower) and for
+        // small problems (configs[1]: 35% slower -- too few blocks to hide the producer); the large-problem test is
+        // >= 8 blocks per SM / CTA pair
         int n_sm = 148;
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, cfg->device);
         const bool auto128 = e128 && (long long)cfg->n_ctrl * (cfg->K / 64) >= 8LL * n_sm && kFuse128Default;
