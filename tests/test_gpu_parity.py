@@ -77,6 +77,9 @@ def test_tc_constructed_relu_net_is_exact(name):
     ("c1pes", {}),                                   # positional encoding, 4 bands
     ("c1pes", {"n_hidden": 4, "activation": 2}),     # PE + SiLU, 3 GEMM layers
     ("c2pes", {}),                                   # PE on the configs[2] MLP (H = 256, CTA pairs)
+    ("c2pes", {"n_hidden": 2}),                      # H = 256 PE layer-1 MMA, 1 GEMM layer
+    ("c2pes", {"n_hidden": 3, "activation": 1}),     # H = 256 PE, 2 GEMM layers, ReLU
+    ("c2pes", {"activation": 0}),                    # H = 256 PE, softplus
 ])
 def test_tc_random_weights_rows(name, over):
     cfg, Ws, bs, inp, ctrl = gh.setup(name, **over)
