@@ -502,15 +502,16 @@ def test_tc_pe_constructed_net(name):
     assert (d > 1e-6).mean() <= 0.05, (d > 1e-6).mean()
 
 
-@pytest.mark.parametrize("name", ["c2s", "c2pes"])
-def test_h256_step_across_controllers(name):
+@pytest.mark.parametrize("name,over", [("c2s", {}), ("c2pes", {}), ("c2pes", {"w_guide": 0.0})])
+def test_h256_step_across_controllers(name, over):
     """H = 256 (CTA-pair tiles of 256 rows) with three controllers of 136 x 5 x 2 = 1360 rows each: pair tiles
     straddle controller boundaries, so the layer-1 epilogue's far-controller path (a row whose folded bias b1'
     belongs to a later controller than the staged one) runs -- for the CUDA-core layer 1 (c2s) and the
-    positional-encoding MMA layer 1 (c2pes). Per-controller latents, gates and goals."""
+    positional-encoding MMA layer 1 (c2pes), with and without the guidance rows. Per-controller latents, gates and
+    goals (PAPER.md:40, :168)."""
     from tests.test_gpu_parity import _bf16_step_checks
-    cfg, Ws, bs, inp, ctrl = gh.setup(name, n_ctrl=3)
-    assert (cfg.K * cfg.T * 2) % 256 != 0
+    cfg, Ws, bs, inp, ctrl = gh.setup(name, n_ctrl=3, **over)
+    assert (cfg.K * cfg.T * (2 if cfg.fd else 1)) % 256 != 0   # (without guidance: one row per state)
     ctrl.step(inp["x0"], inp["goal"], 0)
     ref = gh.run_oracle(cfg, Ws, bs, inp)
     _bf16_step_checks(cfg, Ws, bs, inp, ctrl, ref)
