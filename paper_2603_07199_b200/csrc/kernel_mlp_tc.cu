@@ -100,6 +100,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #define MPPI_DESC_ADD -1   // TS-form K-step B descriptors by one 32-bit add on the address field: -1 = with PE only
                           // (A/B: configs[2]+PE -1.5%, configs[2] +0.3%, configs[3] -0.2%), 0 / 1 = off / on
 #endif
+#ifndef MPPI_FUSE_CTL
+#define MPPI_FUSE_CTL 80   // FUSE: registers of the control warpgroup (the rollout producers); the epilogue gets the rest
+#endif
 #ifndef MPPI_PE_MMA
 #define MPPI_PE_MMA 1   // H = 256 with PE: the 27 position features as a K = 96 exact-split MMA (Cfg::L1PE)
 #endif
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C = Cfg<H, G, PEB>;
     static_assert(!FUSE || (H == 256 && PEB == 0 && !C::L1M), "fused rollout: H = 256 CTA pairs, CUDA-core layer 1");
     // FUSE: the producer warps share warpgroup 0 with the issuer and need ~80 registers (no epilogue spills at 96)
-    constexpr int kCtl = FUSE ? 80 : kRegsCtl;
+    constexpr int kCtl = FUSE ? MPPI_FUSE_CTL : kRegsCtl;
     constexpr int kEpi = ((96 * 640 - 128 * kCtl) / 512) / 8 * 8;
     constexpr int CG = C::CG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
