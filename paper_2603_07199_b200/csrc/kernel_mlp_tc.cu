@@ -103,6 +103,9 @@ constexpr int kCW = 16;         // TMEM columns per epilogue load
 #ifndef MPPI_FUSE_CTL
 #define MPPI_FUSE_CTL 80   // FUSE: registers of the control warpgroup (the rollout producers); the epilogue gets the rest
 #endif
+#ifndef MPPI_BIAS_EPI
+#define MPPI_BIAS_EPI 0   // 1: hidden biases added in the epilogue (FFMA2) instead of one K = 16 ones x bias MMA per unit
+#endif
 #ifndef MPPI_PE_MMA
 #define MPPI_PE_MMA 1   // H = 256 with PE: the 27 position features as a K = 96 exact-split MMA (Cfg::L1PE)
 #endif
@@ -138,7 +141,12 @@ struct Cfg {
     static constexpr int K1_USED = 18 + 18 * PEB;                     // layer-1 operand columns in use
     static constexpr int K1 = (K1_USED + 15) / 16 * 16;              // 32, or 96 with 4 PE bands
     static constexpr int K1S = K1 / 16;                              // K = 16 MMA steps of layer 1
-    static constexpr bool BIAS_MMA = !L1PE;                          // hidden biases by a ones x bias MMA
+    static constexpr bool BIAS_MMA = !MPPI_BIAS_EPI;                 // hidden biases by a ones x bias MMA
+    // L1PE: the bias operands in compact form, built at kernel start: per layer l an 8-row ones tile with the ones
+    // in K columns 2l, 2l+1, read with SBO = 0 (every 8-row group the same rows), and per N-half ONE bias image
+    // holding all layers, b_hi / b_lo of layer l in columns 2l, 2l+1 -- 4.8 KB instead of 16 KB (the 24 KB layer-1
+    // B operand needs the rest). Biases in the epilogue instead (MPPI_BIAS_EPI) measured +7% / +10.6% at H = 256.
+    static constexpr bool BIAS_COMPACT = L1PE && BIAS_MMA;
     static constexpr int NROWBUF = L1PE ? 0 : L1M ? NSLOT : 2 * NSLOT;   // query-row buffers (L1M: |v| in registers)
     static constexpr int QW = UN / COLG;                     // epilogue columns per warp per unit
     static constexpr int NCH = QW / kCW;                     // TMEM loads per warp per unit
@@ -158,10 +166,11 @@ struct Cfg {
     // kP-scaled fp32 bias), both no-swizzle K-major -- so the epilogue adds nothing
     static constexpr int BIAS_UNIT = RB * 32;                        // RB rows x 16 bf16
     static constexpr int IMG_BYTES = W_BYTES + G * NH * BIAS_UNIT;   // weight image per CTA (rank), global stride
-    static constexpr int BIAS_BYTES = BIAS_MMA ? G * NH * BIAS_UNIT : 0;   // bias images in shared memory
+    static constexpr int BIAS_BYTES = BIAS_MMA ? (BIAS_COMPACT ? NH : G * NH) * BIAS_UNIT : 0;   // bias images (smem)
     static constexpr int OFF_BIAS = W_BYTES;
-    static constexpr int OFF_ONES = OFF_BIAS + BIAS_BYTES;           // [128 rows][16] bf16 ones tile
-    static constexpr int OFF_HB = OFF_ONES + (BIAS_MMA ? kTileRows * 32 : 0);   // !BIAS_MMA: [G][H] kP b (fp32)
+    static constexpr int OFF_ONES = OFF_BIAS + BIAS_BYTES;           // [128 rows][16] bf16 ones tile (compact: [G][8][16])
+    static constexpr int ONES_BYTES = BIAS_COMPACT ? G * 256 : kTileRows * 32;
+    static constexpr int OFF_HB = OFF_ONES + (BIAS_MMA ? ONES_BYTES : 0);   // !BIAS_MMA: [G][H] kP b (fp32)
     static constexpr int OFF_WO = OFF_HB + (BIAS_MMA ? 0 : 4 * G * H);         // [H] output weights
     static constexpr int OFF_W1XY = OFF_WO + 4 * H;                  // [H/2] (w0x, w1x, w0y, w1y) layer-1 positions, scaled
     static constexpr int OFF_W1Z = OFF_W1XY + (L1M ? 0 : 8 * H);     // [H/2] (w0z, w1z)
@@ -178,7 +187,7 @@ struct Cfg {
     static constexpr int OFF_SA = A1S ? (OFF_ROWS + NROWBUF * 16 * kTileRows + 1023) / 1024 * 1024 : 0;
     static constexpr int SA_BYTES = kTileRows * H * 2;               // [K/64][128 rows][128 B] SW128 K-major
     static constexpr int OFF_BAR = A1S ? OFF_SA + NSLOT * SA_BYTES : OFF_ROWS + NROWBUF * 16 * kTileRows;
-    static constexpr int OFF_TMEM = OFF_BAR + 8 * 32;
+    static constexpr int OFF_TMEM = OFF_BAR + 8 * (L1PE ? 28 : 32);   // L1PE: no FUSE barriers (<= BAR_AK0 + 1)
     static constexpr int SMEM = 1024 + OFF_TMEM + 16;
     static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -317,7 +326,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* s_hb = reinterpret_cast<float*>(smem + C::OFF_HB);
         for (int i = threadIdx.x; i < G * H; i += kThreads) s_hb[i] = hid_b[i] * kP;
     }
-    if constexpr (C::BIAS_MMA)
+    if constexpr (C::BIAS_COMPACT) {
+        uint32_t* zb = reinterpret_cast<uint32_t*>(smem + C::OFF_BIAS);   // bias images and ones tiles are adjacent
+        for (int i = threadIdx.x; i < (C::BIAS_BYTES + C::ONES_BYTES) / 4; i += kThreads) zb[i] = 0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < G * 8; i += kThreads)   // ones tile l, row r: K columns 2l, 2l+1
+            *reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (i / 8) * 256 + (i % 8) * 16 + (i / 8) * 4) = 0x3F803F80u;
+        for (int idx = threadIdx.x; idx < C::NH * C::RB; idx += kThreads) {   // bias image of N-half q, neuron nn
+            const int q = idx / C::RB, nn = idx % C::RB;
+            const int n = q * C::UN + (int)rank * C::RB + nn;
+            for (int l = 0; l < G; ++l) {   // the bf16 split of kP b (as the global image's, mlp_tc_pack_weights)
+                const float bv = hid_b[l * H + n] * kP;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(bv);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(bv - __bfloat162float(hi));
+                *reinterpret_cast<uint32_t*>(smem + C::OFF_BIAS + q * C::BIAS_UNIT + (nn / 8) * 256 + ((2 * l) / 8) * 128 +
+                                             (nn % 8) * 16 + ((2 * l) % 8) * 2) =
+                    (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+            }
+        }
+    } else if constexpr (C::BIAS_MMA)
     for (int r = threadIdx.x; r < kTileRows; r += kThreads) {   // ones tile: row r = [1, 1, 0 x 14] (bf16)
         uint32_t* o = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES + (r / 8) * 256 + (r % 8) * 16);
         o[0] = 0x3F803F80u;
@@ -367,12 +394,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 1) {
         // ================= weight loader: this CTA's share of every unit, once
         if (lane == 0 && group < n_tiles) {
-            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)(C::W_BYTES + C::BIAS_BYTES));
+            mbar_expect_tx(bar(BAR_WLOCAL), (uint32_t)(C::W_BYTES + (C::BIAS_COMPACT ? 0 : C::BIAS_BYTES)));
             const uint8_t* src = wimg + (size_t)rank * C::IMG_BYTES;
             for (int u = 0; u < G * C::NH; ++u)
                 bulk_g2s(sbase + (uint32_t)(u * C::UNIT_BYTES), src + (size_t)u * C::UNIT_BYTES, C::UNIT_BYTES,
                          bar(BAR_WLOCAL));
-            if constexpr (C::BIAS_MMA)
+            if constexpr (C::BIAS_MMA && !C::BIAS_COMPACT)
                 bulk_g2s(sbase + (uint32_t)C::OFF_BIAS, src + C::W_BYTES, C::BIAS_BYTES, bar(BAR_WLOCAL));
             mbar_wait(bar(BAR_WLOCAL), 0);
             if constexpr (CG == 2) mbar_arrive_cluster(lbar(BAR_WREADY));
@@ -519,7 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int j_mid = C::SPLITK && h == 0 ? H / 32 : H / 16;
                             if (!kWarpIssuer || elect_one()) {
                                 // D = bias (ones x [b_hi, b_lo]), then D += A W^T over K = H
-                                if constexpr (C::BIAS_MMA)
+                                if constexpr (C::BIAS_COMPACT)
+                                    tc_mma_ss<CG>(d_t, smem_desc_noswz(sbase + (uint32_t)(C::OFF_ONES + l * 256), 128, 0),
+                                                  smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + h * C::BIAS_UNIT)),
+                                                  idesc, 0u);
+                                else if constexpr (C::BIAS_MMA)
                                     tc_mma_ss<CG>(d_t, smem_desc_kmajor_noswz(sbase + (uint32_t)C::OFF_ONES),
                                                   smem_desc_kmajor_noswz(sbase + (uint32_t)(C::OFF_BIAS + (l * C::NH + h) * C::BIAS_UNIT)),
                                                   idesc, 0u);
